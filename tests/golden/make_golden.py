@@ -1,0 +1,214 @@
+"""Generate the golden parity fixtures by running the REFERENCE implementation.
+
+Run in the dev container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Every array written here is an output of the unmodified reference package
+(`tilesampler`, /root/reference/pkg/src/tilesampler).  The fixtures are
+committed so that the GPU box (which has no /root/reference) can check the
+CUDA library and the C oracle against them.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import tilesampler as ts  # noqa: E402
+from tilesampler import rng  # noqa: E402
+from tilesampler.cftp import chain_master_seed, schedule_seed  # noqa: E402
+from tilesampler.lozenge import LozengeTiling, loz_random_walk_batch  # noqa: E402
+from tilesampler.sixvertex import sv_random_walk_batch  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, ".."))
+import golden_cases as gc  # noqa: E402  (shared case definitions)
+
+
+def fp(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def save(name: str, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name}: {os.path.getsize(path)} B")
+
+
+# ---------------------------------------------------------------- RNG KATs
+def make_rng():
+    kats = []
+    for seed, shape, site, step in gc.RNG_KATS:
+        fam = ts.seed_family(seed, shape)
+        key = fam.site_key(site)
+        x = rng._splitmix_at(key, step)
+        u = fam.uniform(site, step)
+        g = fam.global_uniform(step)
+        kats.append(
+            dict(seed=seed, shape=list(shape), site=list(site), step=step,
+                 key=key, x=x, u=u.hex(), global_u=g.hex())
+        )
+    derives = [
+        dict(seed=s, index=i, salt=salt, out=rng.derive_seed(s, i, salt))
+        for s, i, salt in gc.DERIVE_KATS
+    ]
+    sched = [dict(master=m, k=k, chain=chain_master_seed(m, k),
+                  round1=schedule_seed(chain_master_seed(m, k), 1))
+             for m, k in gc.CHAIN_KATS]
+    grids = {}
+    for seed, shape, step in gc.GRID_KATS:
+        grids[f"{seed}_{shape[0]}_{shape[1]}_{step}"] = ts.seed_family(seed, shape).uniform_grid(step)
+    with open(os.path.join(HERE, "rng_kats.json"), "w") as f:
+        json.dump(dict(kats=kats, derive=derives, chains=sched), f, indent=1)
+    save("rng_grids.npz", **grids)
+
+
+# ----------------------------------------------------------- domino walks
+def make_domino():
+    # C1 (BASELINE config 1): Aztec order 64, T_max, seed 0x5EED, 1000 sweeps
+    d = ts.Domain.aztec(64)
+    t_max, t_min = ts.extremal_tilings(d)
+    plan = ts.SweepPlan(d)
+    out = ts.random_walk(t_max, 0x5EED, 1000, plan)
+    h = ts.height_function(out).heights
+    print("C1 states", fp(out.states), "heights", fp(h), "t_max", fp(t_max.states))
+    save("domino_c1.npz", t_max=t_max.states, t_min=t_min.states, final=out.states,
+         heights=h, heights_tmax=ts.height_function(t_max).heights)
+
+    arrays = {}
+    for i, case in enumerate(gc.domino_walk_cases()):
+        d, plan, start = case["domain"], case["plan"], case["start"]
+        states = np.stack(start)
+        seeds = np.asarray(case["seeds"], dtype=np.uint64)
+        res = ts.random_walk_batch(states, seeds, case["n_steps"], plan)
+        arrays[f"c{i}_faces"] = d.faces
+        arrays[f"c{i}_start"] = states
+        arrays[f"c{i}_seeds"] = seeds
+        arrays[f"c{i}_n_steps"] = np.array(case["n_steps"])
+        arrays[f"c{i}_p_up"] = plan.p_up
+        arrays[f"c{i}_out"] = res
+    # single sweeps with an explicit colour/step (sweeps.py:322-342)
+    for j, (dom, seed, step, color) in enumerate(gc.SWEEP_CASES):
+        d = dom()
+        plan = ts.SweepPlan(d)
+        t0 = ts.random_walk(ts.extremal_tilings(d)[0], 77 + j, 40, plan)
+        fam = ts.seed_family(seed, (d.n + 1, d.n + 1))
+        t1, rot = ts.sweep(t0, fam, step, ts.Color(color), plan, return_rotated=True)
+        arrays[f"s{j}_faces"] = d.faces
+        arrays[f"s{j}_in"] = t0.states
+        arrays[f"s{j}_out"] = t1.states
+        arrays[f"s{j}_rot"] = rot
+    save("domino_walks.npz", **arrays)
+
+
+# ------------------------------------------------ extremal tilings, heights
+def make_extremal():
+    arrays = {}
+    for i, d in enumerate(gc.extremal_domains()):
+        arrays[f"d{i}_faces"] = d.faces
+        ext = ts.extremal_tilings(d)
+        if ext is None:
+            arrays[f"d{i}_none"] = np.array(1)
+            continue
+        t_max, t_min = ext
+        arrays[f"d{i}_tmax"] = t_max.states
+        arrays[f"d{i}_tmin"] = t_min.states
+        arrays[f"d{i}_hmax"] = ts.height_function(t_max).heights
+        arrays[f"d{i}_hmin"] = ts.height_function(t_min).heights
+        arrays[f"d{i}_ref"] = np.array(d.reference_vertex)
+        arrays[f"d{i}_vmask"] = d.vertex_mask
+        # a mixed tiling and its heights
+        mixed = ts.random_walk(t_max, 1000 + i, 60, ts.SweepPlan(d))
+        arrays[f"d{i}_mixed"] = mixed.states
+        arrays[f"d{i}_hmixed"] = ts.height_function(mixed).heights
+    save("domino_extremal.npz", **arrays)
+
+
+# ------------------------------------------------------------------- CFTP
+def make_cftp():
+    arrays = {}
+    meta = []
+    for i, (dom, weights, master, count, maxd) in enumerate(gc.CFTP_CASES):
+        d = dom()
+        plan = ts.SweepPlan(d, weights)
+        trace = ts.CftpTrace()
+        samples = ts.cftp_sample_many(d, plan, master, count, max_doublings=maxd, trace=trace)
+        arrays[f"k{i}_faces"] = d.faces
+        arrays[f"k{i}_samples"] = np.stack([s.states for s in samples])
+        meta.append(dict(rounds=[[list(p) for p in r] for r in trace.rounds],
+                         collapsed_at=trace.collapsed_at))
+    save("domino_cftp.npz", **arrays)
+    with open(os.path.join(HERE, "domino_cftp_traces.json"), "w") as f:
+        json.dump(meta, f)
+
+
+# ------------------------------------------------------------- six-vertex
+def make_sixvertex():
+    arrays = {}
+    for i, (n, weights, seed, n_steps, start) in enumerate(gc.SV_CASES):
+        b = ts.dwbc(n)
+        hi, lo = ts.sv_extremal(n, b)
+        h0 = (hi if start == "max" else lo).heights
+        out = sv_random_walk_batch(h0[None], np.array([seed], dtype=np.uint64), n_steps,
+                                   ts.SVWeights(*weights))
+        arrays[f"v{i}_start"] = h0
+        arrays[f"v{i}_out"] = out[0]
+        arrays[f"v{i}_table"] = ts.SVWeights(*weights).table()
+        print(f"sv case {i} n={n} w={weights} -> {fp(out[0])}")
+    for n in gc.SV_EXTREMAL_N:
+        hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+        arrays[f"e{n}_hi"] = hi.heights
+        arrays[f"e{n}_lo"] = lo.heights
+    # CFTP on DWBC 3 / 4
+    for j, (n, weights, master, count) in enumerate(gc.SV_CFTP_CASES):
+        trace = ts.CftpTrace()
+        res = ts.sv_cftp(n, ts.dwbc(n), ts.SVWeights(*weights), master, count=count, trace=trace)
+        res = res if isinstance(res, list) else [res]
+        arrays[f"k{j}_h"] = np.stack([ts.heights_from_config(c).heights for c in res])
+        arrays[f"k{j}_collapsed"] = np.array(trace.collapsed_at)
+    save("sixvertex.npz", **arrays)
+
+
+# ---------------------------------------------------------------- lozenges
+def make_lozenge():
+    arrays = {}
+    for i, (abc, weights, seed, n_steps, start) in enumerate(gc.LOZ_CASES):
+        dom = ts.TriDomain.hexagon(*abc)
+        t_max, t_min = ts.loz_extremal(dom)
+        t0 = t_max if start == "max" else t_min
+        out = loz_random_walk_batch(t0.edges[None], np.array([seed], dtype=np.uint64),
+                                    n_steps, dom, weights)
+        tout = LozengeTiling(dom, out[0])
+        arrays[f"l{i}_start"] = t0.edges
+        arrays[f"l{i}_out"] = out[0]
+        arrays[f"l{i}_heights"] = ts.loz_heights(tout).heights
+        from tilesampler.lozenge import loz_p_up_grid
+        arrays[f"l{i}_p_up"] = loz_p_up_grid(dom, weights)
+        print(f"loz case {i} {abc} -> edges {fp(out[0])} heights {fp(arrays[f'l{i}_heights'])}")
+    for abc in gc.LOZ_EXTREMAL:
+        dom = ts.TriDomain.hexagon(*abc)
+        t_max, t_min = ts.loz_extremal(dom)
+        key = "x" + "_".join(map(str, abc))
+        arrays[key + "_max"] = t_max.edges
+        arrays[key + "_min"] = t_min.edges
+        arrays[key + "_hmax"] = ts.loz_heights(t_max).heights
+        arrays[key + "_hmin"] = ts.loz_heights(t_min).heights
+    for j, (abc, master, count) in enumerate(gc.LOZ_CFTP_CASES):
+        dom = ts.TriDomain.hexagon(*abc)
+        res = ts.loz_cftp(dom, ts.Uniform(), master, count=count)
+        res = res if isinstance(res, list) else [res]
+        arrays[f"k{j}_edges"] = np.stack([t.edges for t in res])
+    save("lozenge.npz", **arrays)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge"]
+    for w in which:
+        globals()[f"make_{w}"]()
