@@ -1,0 +1,132 @@
+/*
+ * tsb.h -- C ABI of the B200 (sm_100a) tilesampler library, libtsb.so.
+ *
+ * Drop-in boundary for the reference `tilesampler` hot path (colour-class
+ * Glauber sweeps + CFTP).  Plain pointers and sizes only; host buffers use the
+ * reference's own layouts and dtypes, so a binding is a few ctypes lines
+ * (see INTEGRATION.md).  Reference paths are relative to
+ * /root/reference/pkg/src/tilesampler/.
+ *
+ * Conventions
+ *  - Every entry point returns a status (0 = OK).  Non-zero codes map to the
+ *    reference exception taxonomy (errors.py:4-69); tsb_last_error() gives the
+ *    message of the calling thread's last failure.
+ *  - Handles own device memory; callers own host buffers.  A handle is used by
+ *    one host thread at a time; distinct handles are independent.
+ *  - Work is enqueued on the handle's stream (tsb_*_set_stream to share a
+ *    torch stream).  *_download and *_sync synchronise that stream.
+ *  - Chain k's result depends only on its own seed, never on batching or on
+ *    which device ran it (reference contract sweeps.py:286-292, cftp.py:11-14).
+ *  - There is no CPU fallback: without an sm_100 device every call fails
+ *    with TSB_E_NODEVICE.
+ */
+#ifndef TSB_H
+#define TSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TSB_OK = 0,
+    TSB_E_VALUE = 1,        /* ValueError                                     */
+    TSB_E_INCONSISTENT = 2, /* InconsistencyError   (errors.py:24-25)         */
+    TSB_E_CAPACITY = 3,     /* CapacityError        (errors.py:32-33)         */
+    TSB_E_CUDA = 4,         /* RuntimeError: CUDA failure                     */
+    TSB_E_NODEVICE = 5,     /* RuntimeError: no sm_100 device                 */
+    TSB_E_CONVERGENCE = 6,  /* ConvergenceCapExceeded (errors.py:64-65)       */
+    TSB_E_DOMAIN = 7,       /* DomainError          (errors.py:8-9)           */
+    TSB_E_UNTILEABLE = 8    /* UntileableDomain     (errors.py:56-57)         */
+};
+
+/* ---------------------------------------------------------------- library */
+const char *tsb_last_error(void);
+int tsb_abi_version(void);
+/* SM count, compute capability and L2 size of `device`. */
+int tsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor, int64_t *l2_bytes);
+
+/* ------------------------------------------------------------------- RNG */
+/* StreamFamily(seed, (rows, cols)).uniform_grid(step, tag) -> out[rows*cols]
+ * float64, computed on the device.  Replaces rng.py:105-123 (and the batched
+ * key_grid_batch/uniform_from_keys, rng.py:138-162).  Host output buffer. */
+int tsb_uniform_grid(int device, uint64_t seed, int rows, int cols, uint64_t step, int tag,
+                     double *out);
+
+/* --------------------------------------------------------------- dominoes */
+typedef struct tsb_domino tsb_domino;
+
+/* A batch of `nchains` domino chains on the (side x side) vertex grid,
+ * side = Domain.n + 1 (lattice.py:267-280).  `faces` is the Domain.faces
+ * grid ((side-1) x (side-1), uint8/bool, row-major) or NULL for the full box;
+ * it bounds the work region and the crossable edges. */
+int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, tsb_domino **out);
+int tsb_domino_destroy(tsb_domino *h);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+int tsb_domino_set_stream(tsb_domino *h, void *stream);
+/* SweepPlan.p_up, (side x side) float64 (sweeps.py:170-179).  Converted
+ * exactly to integer thresholds: u < p  <=>  (x >> 11) < ceil(p * 2^53). */
+int tsb_domino_set_p_up(tsb_domino *h, const double *p_up);
+
+/* Tiling.states batch (n, side, side) uint8 <-> device state.  Upload
+ * rejects grids that are not edge-consistent or that cross a non-crossable
+ * edge with TSB_E_INCONSISTENT. */
+int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states);
+int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states);
+
+/* n_steps sweeps of chains [chain0, chain0+n) with per-chain seeds, step
+ * counter starting at step0 (the reference always uses step0 = 0; a walk of
+ * a+b steps equals a walk of a steps followed by one of b steps at step0=a).
+ * Replaces the fused hook _fused_walk(out, site_keys, global_keys, p_up,
+ * n_steps) (sweeps.py:272-275, 306-309; _kernels.py:35-69), with seeds in
+ * place of the materialised key grids (keys are derived on the device). */
+int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step0,
+                    uint64_t n_steps);
+/* One sweep with an explicit colour (0 = BLACK, 1 = WHITE) at `step`
+ * (sweeps.py:322-342). */
+int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step,
+                     int color);
+int tsb_domino_sync(tsb_domino *h);
+
+/* Height function of chain `chain` (lattice.py:537-580): int32 (side x side),
+ * 0 outside Domain.vertex_mask, h(ref) = 0 at the reference vertex
+ * (lattice.py:197-203).  TSB_E_INCONSISTENT when the state does not
+ * integrate. */
+int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *out);
+/* Thurston's maximal / minimal tilings of the handle's domain written into
+ * chains chain_max / chain_min (lattice.py:734-754).  TSB_E_UNTILEABLE when
+ * the domain has no tiling (the reference returns None). */
+int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, int ref_c);
+
+/* ------------------------------------------------------------------ CFTP */
+/* Progress callback: (round, steps = sum_{i<=round} 2^i, samples collapsed so
+ * far, batch size, user) -- the reference's progress hook (cftp.py:130-136). */
+typedef void (*tsb_progress_fn)(int round_no, uint64_t steps, int collapsed, int total, void *user);
+
+/* K7: flags[j] = 1 iff chains chain0+2j and chain0+2j+1 hold identical states
+ * (collapse_check / (top == bot).all(), cftp.py:71-75, 120). */
+int tsb_domino_coalesced(tsb_domino *h, int chain0, int npairs, uint8_t *flags);
+/* Copy chain `src` into chains dst0, dst0+step, ... (n copies). */
+int tsb_domino_replicate(tsb_domino *h, int src, int dst0, int step, int n);
+/* Monotone CFTP for `count` samples with chain master seeds `masters`
+ * (cftp_sample_many / run_cftp_batch, cftp.py:86-139, 161-213): doubling
+ * rounds, pair seeds derive_seed(m, r, 0x51ED2701), newest pair first, each
+ * round restarted from top0 (T_max) / bot0 (T_min) host grids.  Writes the
+ * coalesced bottom state of sample k to out_states[k] ((count, side, side)
+ * uint8) and the round it collapsed in to collapsed_round[k] (nullable).
+ * Needs nchains >= 2*count + 2.  TSB_E_CONVERGENCE after max_doublings. */
+int tsb_domino_cftp(tsb_domino *h, const uint8_t *top0, const uint8_t *bot0, const uint64_t *masters,
+                    int count, int max_doublings, uint8_t *out_states, int32_t *collapsed_round,
+                    tsb_progress_fn progress, void *user);
+
+/* One-shot form of the fused hook: evolves a host (nchains, side, side)
+ * uint8 batch in place (upload + walk + download). */
+int tsb_domino_walk_host(int device, uint8_t *states, int nchains, int side, const uint64_t *seeds,
+                         const double *p_up, const uint8_t *faces, uint64_t n_steps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSB_H */

@@ -1,0 +1,548 @@
+// Domino tilings: bit-plane state, colour-class Glauber sweep, codecs.
+//
+// Reference path (relative to /root/reference/pkg/src/tilesampler/):
+//   _kernels.py:35-69  domino_walk   (the fused CPU kernel this replaces)
+//   sweeps.py:209-316  sweep_batch / random_walk_batch
+//   lattice.py:51-61, 267-280  tilestate bits and the Tiling grid
+//
+// Device state (per chain): two bit planes over the (side x side) vertex grid,
+// interleaved as one uint2 {V, H} per (row, 32-column word):
+//   V[r] bit c  = vertical edge (r,c)-(r+1,c) crossed  (= "down" bit 2 of (r,c)
+//                 = "up" bit 1 of (r+1,c))
+//   H[r] bit c  = horizontal edge (r,c)-(r,c+1) crossed (= "right" bit 8 of
+//                 (r,c) = "left" bit 4 of (r,c+1))
+// Each edge is stored once: 2 bits per vertex instead of the reference's
+// 8-bit tilestate.  Rows -1 and `side` are zero guard rows.  The tilestate of
+// (r,c) is  V[r-1]c | V[r]c << 1 | H[r]c-1 << 2 | H[r]c << 3.
+//
+// A sweep of colour `col` rotates every active vertex ((r+c)%2 == col) whose
+// state is 3 (V[r-1],V[r] set, H[r]c-1,H[r]c clear) or 12 (the reverse) with
+// its own (site, step) coin; a rotation toggles its four incident edges.  The
+// reference's "update the other colour" pass is implicit: the other colour's
+// tilestates are read off the same edges.  Same-colour vertices share no
+// edge, so a sweep is a pure function of the previous state and is computed
+// out of place (double buffer).
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "domino.cuh"
+
+namespace tsb {
+
+constexpr int kBand = 16;          // rows marched by one warp
+constexpr int kWarpsPerBlock = 4;  // warps per block (stacked bands)
+
+struct SweepCtx {
+    const uint2 *src;
+    uint2 *dst;
+    const int2 *range;         // [side] word range [lo, hi) that can hold set bits
+    const uint64_t *seedinfo;  // [n][2] = {family base, global key}
+    const uint64_t *tgrid;     // per-site thresholds (mode 2), (side x side)
+    uint64_t t0, t1;           // thresholds for even / odd parity (modes 0, 1)
+    size_t chain_stride;       // uint2 per chain (incl. guard rows)
+    int side, W, pitch;
+    uint64_t step;
+    int color_override;  // -1: colour from the global coin
+};
+
+// Fire mask of one 32-column word: bit b set iff the active vertex at column
+// 32*w+b is rotateable and its heat-bath coin moves it (3 -> 12 when
+// u < p_up, 12 -> 3 otherwise; _kernels.py:49-55, sweeps.py:102-110).
+template <int TM>
+__device__ __forceinline__ uint32_t fire_word(uint32_t vu, uint32_t vd, uint32_t h, uint32_t hleft,
+                                              uint32_t act, int r, int w, uint64_t base,
+                                              uint64_t salt, int color, const SweepCtx &c) {
+    const uint32_t l = (h << 1) | (hleft >> 31);
+    const uint32_t is3 = vu & vd & ~(l | h) & act;
+    const uint32_t is12 = ~(vu | vd) & l & h & act;
+    uint32_t rot = is3 | is12;
+    uint32_t fire = 0;
+    while (rot) {
+        const int b = __ffs(rot) - 1;
+        rot &= rot - 1;
+        const uint64_t idx = (uint64_t)r * (uint64_t)c.side + (uint64_t)(w * 32 + b);
+        const uint64_t x = mix64(mix64(base + (idx + 1ull) * kGold) + salt);
+        uint64_t t;
+        if (TM == 0) t = c.t0;
+        else if (TM == 1) t = color ? c.t1 : c.t0;
+        else t = __ldg(c.tgrid + idx);
+        const bool up = (x >> 11) < t;
+        if (up == (bool)((is3 >> b) & 1u)) fire |= 1u << b;
+    }
+    return fire;
+}
+
+__device__ __forceinline__ uint2 ld_word(const uint2 *row, int w, int2 rg) {
+    return (w >= rg.x && w < rg.y) ? __ldg(row + w) : make_uint2(0u, 0u);
+}
+
+// One sweep.  Warp = 32 consecutive words of one row band; it marches down
+// kBand rows keeping rows r-1, r, r+1 in registers, so every fire row is
+// computed once per band (plus one halo row).  Horizontal neighbours come
+// from lane shuffles; lane 0 / lane 31 fetch the words beyond the warp.
+template <int TM>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    domino_sweep_kernel(SweepCtx c) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int w = blockIdx.x * 32 + lane;
+    const int r0 = (blockIdx.y * kWarpsPerBlock + warp) * kBand;
+    if (r0 >= c.side) return;  // warp-uniform
+    const int r1 = min(r0 + kBand, c.side);
+    const int2 *range = c.range;
+
+    // Skip warps whose words never hold set bits in this band.
+    {
+        int lo = INT_MAX, hi = INT_MIN;
+        if (lane < r1 - r0) {
+            int2 rg = __ldg(range + r0 + lane);
+            if (rg.y > rg.x) { lo = rg.x; hi = rg.y; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        const int w0 = blockIdx.x * 32;
+        if (hi <= w0 || lo >= w0 + 32) return;  // warp-uniform
+    }
+
+    const int z = blockIdx.z;
+    const uint2 *src = c.src + (size_t)z * c.chain_stride + c.pitch;  // row 0
+    uint2 *dst = c.dst + (size_t)z * c.chain_stride + c.pitch;
+    const uint64_t base = c.seedinfo[2 * z];
+    const uint64_t gkey = c.seedinfo[2 * z + 1];
+    const uint64_t salt = (c.step + 1ull) * kGold;
+    // colour coin: BLACK iff u < 1/2  <=>  bit 63 of the draw is 0
+    // (_kernels.py:44-45, sweeps.py:266-269)
+    const int color = c.color_override >= 0 ? c.color_override : (int)(mix64(gkey + salt) >> 63);
+    const bool l0 = lane == 0, l31 = lane == 31;
+    const int2 zero2 = make_int2(0, 0);
+
+    auto rg_of = [&](int r) -> int2 { return (r >= 0 && r < c.side) ? __ldg(range + r) : zero2; };
+    auto act_of = [&](int r) -> uint32_t { return ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u; };
+
+    // prologue: row r0-1 (V only) and row r0
+    int2 rgm = rg_of(r0 - 1);
+    int2 rg0 = rg_of(r0);
+    uint32_t vm1 = ld_word(src + (size_t)(r0 - 1) * c.pitch, w, rgm).x;
+    uint2 t = ld_word(src + (size_t)r0 * c.pitch, w, rg0);
+    uint32_t v0 = t.x, h0 = t.y;
+    uint32_t hl = __shfl_up_sync(0xffffffffu, h0, 1);
+    if (l0) hl = ld_word(src + (size_t)r0 * c.pitch, w - 1, rg0).y;
+    // lane 31 also tracks word w+1 (only its bit 0 matters)
+    uint32_t xv0 = 0, xh0 = 0, xvm1 = 0;
+    if (l31) {
+        xvm1 = ld_word(src + (size_t)(r0 - 1) * c.pitch, w + 1, rgm).x;
+        uint2 tx = ld_word(src + (size_t)r0 * c.pitch, w + 1, rg0);
+        xv0 = tx.x;
+        xh0 = tx.y;
+    }
+    uint32_t a0 = act_of(r0);
+    uint32_t f0 = fire_word<TM>(vm1, v0, h0, hl, a0, r0, w, base, salt, color, c);
+    uint32_t fx0 = l31 ? fire_word<TM>(xvm1, xv0, xh0, h0, a0 & 1u, r0, w + 1, base, salt, color, c) : 0u;
+
+    for (int r = r0; r < r1; ++r) {
+        const int2 rgn = rg_of(r + 1);
+        const uint2 *rown = src + (size_t)(r + 1) * c.pitch;
+        uint2 tn = ld_word(rown, w, rgn);
+        const uint32_t v1 = tn.x, h1 = tn.y;
+        uint32_t hl1 = __shfl_up_sync(0xffffffffu, h1, 1);
+        if (l0) hl1 = ld_word(rown, w - 1, rgn).y;
+        uint32_t xv1 = 0, xh1 = 0;
+        if (l31) {
+            uint2 tx = ld_word(rown, w + 1, rgn);
+            xv1 = tx.x;
+            xh1 = tx.y;
+        }
+        const uint32_t a1 = act_of(r + 1);
+        const uint32_t f1 = fire_word<TM>(v0, v1, h1, hl1, a1, r + 1, w, base, salt, color, c);
+        const uint32_t fx1 =
+            l31 ? fire_word<TM>(xv0, xv1, xh1, h1, a1 & 1u, r + 1, w + 1, base, salt, color, c) : 0u;
+        uint32_t fr = __shfl_down_sync(0xffffffffu, f0, 1);
+        if (l31) fr = fx0;
+        const uint32_t nv = v0 ^ f0 ^ f1;
+        const uint32_t nh = h0 ^ f0 ^ (f0 >> 1) ^ (fr << 31);
+        const int2 rgr = rg_of(r);
+        if (w >= rgr.x && w < rgr.y) dst[(size_t)r * c.pitch + w] = make_uint2(nv, nh);
+        v0 = v1;
+        h0 = h1;
+        f0 = f1;
+        xv0 = xv1;
+        xh0 = xh1;
+        fx0 = fx1;
+    }
+}
+
+// --------------------------------------------------------------- codecs
+// Row ranges and crossable-edge planes from Domain.faces
+// (vertex_mask lattice.py:190-195; crossable = both faces of the edge in
+// the domain, lattice.py:67-78, 639-689).
+__device__ __forceinline__ bool face_in(const uint8_t *faces, int nf, int r, int c) {
+    return r >= 0 && c >= 0 && r < nf && c < nf && faces[(size_t)r * nf + c] != 0;
+}
+
+__global__ void domain_planes_kernel(const uint8_t *faces, int side, int W, int pitch,
+                                     uint4 *dom, uint32_t *fbits, int2 *range) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (w >= W) return;
+    const int nf = side - 1;
+    uint32_t cv = 0, ch = 0, ev = 0, eh = 0, fb = 0;
+    bool any = false;
+    for (int b = 0; b < 32; ++b) {
+        const int cc = w * 32 + b;
+        if (cc >= side) break;
+        const bool ful = face_in(faces, nf, r - 1, cc - 1), fur = face_in(faces, nf, r - 1, cc);
+        const bool fdl = face_in(faces, nf, r, cc - 1), fdr = face_in(faces, nf, r, cc);
+        if (ful || fur || fdl || fdr) any = true;
+        if (fdl && fdr) cv |= 1u << b;  // edge down: faces (r,c-1),(r,c)
+        if (fur && fdr) ch |= 1u << b;  // edge right: faces (r-1,c),(r,c)
+        if ((fdl || fdr) && r + 1 < side) ev |= 1u << b;
+        if ((fur || fdr) && cc + 1 < side) eh |= 1u << b;
+        if (fdr) fb |= 1u << b;  // face (r, c)
+    }
+    dom[(size_t)r * pitch + w] = make_uint4(cv, ch, ev, eh);
+    fbits[(size_t)r * pitch + w] = fb;
+    if (any) {
+        atomicMin(&range[r].x, w);
+        atomicMax(&range[r].y, w + 1);
+    }
+}
+
+__global__ void fix_ranges_kernel(int2 *range, int side) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < side && range[r].x >= range[r].y) range[r] = make_int2(0, 0);
+}
+
+// Tiling.states (n, side, side) uint8 -> {V, H} planes, with validation:
+// values < 16, every edge bit mirrored by the neighbour (lattice.py:432-450),
+// no crossed edge leaving the grid or the domain.
+__global__ void pack_kernel(const uint8_t *bytes, int side, int W, int pitch, size_t chain_stride,
+                            const uint4 *dom, uint2 *state, int *bad) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    const int z = blockIdx.z;
+    if (w >= W) return;
+    const uint8_t *g = bytes + (size_t)z * side * side;
+    const uint4 cr = dom[(size_t)r * pitch + w];
+    uint32_t v = 0, h = 0;
+    int err = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int cc = w * 32 + b;
+        if (cc >= side) break;
+        const uint8_t s = g[(size_t)r * side + cc];
+        if (s >= 16) err |= 1;
+        const bool up = s & 1, dn = s & 2, lf = s & 4, rt = s & 8;
+        const bool up_n = r > 0 ? (g[(size_t)(r - 1) * side + cc] & 2) != 0 : false;
+        const bool lf_n = cc > 0 ? (g[(size_t)r * side + cc - 1] & 8) != 0 : false;
+        if (up != up_n || lf != lf_n) err |= 2;
+        if (dn && !((cr.x >> b) & 1u)) err |= 4;
+        if (rt && !((cr.y >> b) & 1u)) err |= 4;
+        if (dn) v |= 1u << b;
+        if (rt) h |= 1u << b;
+    }
+    state[(size_t)z * chain_stride + (size_t)(r + 1) * pitch + w] = make_uint2(v, h);
+    if (err) atomicOr(bad, err);
+}
+
+__global__ void unpack_kernel(const uint2 *state, int side, int pitch, size_t chain_stride,
+                              uint8_t *bytes) {
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    const int z = blockIdx.z;
+    if (cc >= side) return;
+    const uint2 *s = state + (size_t)z * chain_stride + (size_t)(r + 1) * pitch;
+    const int w = cc >> 5, b = cc & 31;
+    const uint32_t up = (s[w - pitch].x >> b) & 1u;
+    const uint32_t dn = (s[w].x >> b) & 1u;
+    const uint32_t rt = (s[w].y >> b) & 1u;
+    const uint32_t lf = cc > 0 ? (s[(cc - 1) >> 5].y >> ((cc - 1) & 31)) & 1u : 0u;
+    bytes[(size_t)z * side * side + (size_t)r * side + cc] = (uint8_t)(up | dn << 1 | lf << 2 | rt << 3);
+}
+
+}  // namespace tsb
+
+using namespace tsb;
+
+namespace tsb {
+
+int ensure_bytes(tsb_domino *h, size_t need) {
+    if (h->bytes_cap >= need) return TSB_OK;
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->bytes) TSB_CUDA(cudaFree(h->bytes));
+    h->bytes = nullptr;
+    TSB_CUDA(cudaMalloc(&h->bytes, need));
+    h->bytes_cap = need;
+    return TSB_OK;
+}
+
+int check_range(tsb_domino *h, int chain0, int n) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    if (chain0 < 0 || n < 0 || chain0 + n > h->nchains)
+        return fail(TSB_E_VALUE, "chains [%d, %d) outside the handle's %d chains", chain0, chain0 + n,
+                    h->nchains);
+    return TSB_OK;
+}
+
+int push_seeds(tsb_domino *h, int n, const uint64_t *seeds) {
+    TSB_CUDA(cudaEventSynchronize(h->seed_ev));  // staging free again
+    for (int i = 0; i < n; ++i) {
+        const uint64_t b = family_base(seeds[i]);
+        h->seed_pinned[2 * i] = b;
+        h->seed_pinned[2 * i + 1] = global_key(b);
+    }
+    TSB_CUDA(cudaMemcpyAsync(h->seedinfo, h->seed_pinned, sizeof(uint64_t) * 2 * n,
+                             cudaMemcpyHostToDevice, h->stream));
+    TSB_CUDA(cudaEventRecord(h->seed_ev, h->stream));
+    return TSB_OK;
+}
+
+int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override) {
+    SweepCtx c;
+    c.src = h->buf[h->cur] + (size_t)chain0 * h->chain_stride;
+    c.dst = h->buf[h->cur ^ 1] + (size_t)chain0 * h->chain_stride;
+    c.range = h->range;
+    c.seedinfo = h->seedinfo;
+    c.tgrid = h->tgrid;
+    c.t0 = h->t0;
+    c.t1 = h->t1;
+    c.chain_stride = h->chain_stride;
+    c.side = h->side;
+    c.W = h->W;
+    c.pitch = h->pitch;
+    c.step = step;
+    c.color_override = color_override;
+    const int nbands = (h->side + kBand - 1) / kBand;
+    dim3 grid((h->W + 31) / 32, (nbands + kWarpsPerBlock - 1) / kWarpsPerBlock, n);
+    dim3 block(32 * kWarpsPerBlock);
+    switch (h->tmode) {
+        case 0: domino_sweep_kernel<0><<<grid, block, 0, h->stream>>>(c); break;
+        case 1: domino_sweep_kernel<1><<<grid, block, 0, h->stream>>>(c); break;
+        default: domino_sweep_kernel<2><<<grid, block, 0, h->stream>>>(c); break;
+    }
+    TSB_CUDA(cudaGetLastError());
+    h->cur ^= 1;
+    return TSB_OK;
+}
+
+// After an odd number of sweeps the walked chains live in the other buffer;
+// copy them back so the handle keeps one canonical buffer for all chains.
+int settle(tsb_domino *h, int chain0, int n, uint64_t nsweeps) {
+    if ((nsweeps & 1) == 0 || n == h->nchains) return TSB_OK;
+    const size_t off = (size_t)chain0 * h->chain_stride;
+    TSB_CUDA(cudaMemcpyAsync(h->buf[h->cur ^ 1] + off, h->buf[h->cur] + off,
+                             sizeof(uint2) * h->chain_stride * n, cudaMemcpyDeviceToDevice, h->stream));
+    h->cur ^= 1;
+    return TSB_OK;
+}
+
+}  // namespace tsb
+
+extern "C" {
+
+int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, tsb_domino **out) {
+    if (!out) return fail(TSB_E_VALUE, "null output pointer");
+    *out = nullptr;
+    if (side < 1 || nchains < 1) return fail(TSB_E_VALUE, "side and nchains must be positive");
+    if ((uint64_t)side * (uint64_t)side >= kCapacity)
+        return fail(TSB_E_CAPACITY, "grid of %lld sites exceeds capacity", (long long)side * side);
+    int rc = ensure_device(device);
+    if (rc) return rc;
+    tsb_domino *h = new tsb_domino();
+    h->device = device;
+    h->side = side;
+    h->nchains = nchains;
+    h->W = (side + 31) / 32;
+    h->pitch = (h->W + 31) / 32 * 32;  // 256-byte aligned rows
+    h->chain_stride = (size_t)(side + 2) * h->pitch;
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaStreamCreate"); }
+    h->own_stream = true;
+    auto bail = [&](cudaError_t err, const char *what) {
+        int code = cuda_fail(err, what);
+        tsb_domino_destroy(h);
+        return code;
+    };
+    const size_t sbytes = sizeof(uint2) * h->chain_stride * nchains;
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaMalloc(&h->buf[i], sbytes)) != cudaSuccess) return bail(e, "cudaMalloc state");
+        if ((e = cudaMemsetAsync(h->buf[i], 0, sbytes, h->stream)) != cudaSuccess) return bail(e, "memset");
+    }
+    if ((e = cudaMalloc(&h->dom, sizeof(uint4) * (size_t)side * h->pitch)) != cudaSuccess)
+        return bail(e, "cudaMalloc dom");
+    if ((e = cudaMalloc(&h->fbits, sizeof(uint32_t) * (size_t)side * h->pitch)) != cudaSuccess)
+        return bail(e, "cudaMalloc fbits");
+    if ((e = cudaMalloc(&h->range, sizeof(int2) * side)) != cudaSuccess) return bail(e, "cudaMalloc range");
+    if ((e = cudaMalloc(&h->seedinfo, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
+        return bail(e, "cudaMalloc seeds");
+    if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
+        return bail(e, "cudaMallocHost seeds");
+    if ((e = cudaMalloc(&h->bad, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc flag");
+    if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess)
+        return bail(e, "cudaEventCreate");
+    if ((e = cudaEventRecord(h->seed_ev, h->stream)) != cudaSuccess) return bail(e, "cudaEventRecord");
+
+    // domain -> crossable planes and row ranges
+    const int nf = side - 1;
+    uint8_t *dfaces = nullptr;
+    const size_t fbytes = std::max<size_t>(1, (size_t)nf * nf);
+    if ((e = cudaMalloc(&dfaces, fbytes)) != cudaSuccess) return bail(e, "cudaMalloc faces");
+    if (faces && nf > 0) e = cudaMemcpyAsync(dfaces, faces, (size_t)nf * nf, cudaMemcpyHostToDevice, h->stream);
+    else e = cudaMemsetAsync(dfaces, 1, fbytes, h->stream);
+    if (e != cudaSuccess) { cudaFree(dfaces); return bail(e, "faces upload"); }
+    std::vector<int2> init(side, make_int2(INT_MAX, INT_MIN));
+    cudaMemcpyAsync(h->range, init.data(), sizeof(int2) * side, cudaMemcpyHostToDevice, h->stream);
+    domain_planes_kernel<<<dim3((h->W + 127) / 128, side), 128, 0, h->stream>>>(dfaces, side, h->W,
+                                                                               h->pitch, h->dom, h->fbits, h->range);
+    fix_ranges_kernel<<<(side + 255) / 256, 256, 0, h->stream>>>(h->range, side);
+    e = cudaStreamSynchronize(h->stream);
+    cudaFree(dfaces);
+    if (e != cudaSuccess) return bail(e, "domain planes");
+    *out = h;
+    return TSB_OK;
+}
+
+int tsb_domino_destroy(tsb_domino *h) {
+    if (!h) return TSB_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    cudaFree(h->buf[0]);
+    cudaFree(h->buf[1]);
+    cudaFree(h->dom);
+    cudaFree(h->fbits);
+    cudaFree(h->range);
+    cudaFree(h->tgrid);
+    cudaFree(h->seedinfo);
+    cudaFree(h->bytes);
+    cudaFree(h->bad);
+    if (h->seed_pinned) cudaFreeHost(h->seed_pinned);
+    if (h->seed_ev) cudaEventDestroy(h->seed_ev);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return TSB_OK;
+}
+
+int tsb_domino_set_stream(tsb_domino *h, void *stream) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    TSB_CUDA(cudaSetDevice(h->device));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    h->stream = (cudaStream_t)stream;
+    h->own_stream = false;
+    return TSB_OK;
+}
+
+int tsb_domino_set_p_up(tsb_domino *h, const double *p_up) {
+    if (!h || !p_up) return fail(TSB_E_VALUE, "null argument");
+    TSB_CUDA(cudaSetDevice(h->device));
+    const int64_t s = h->side;
+    std::vector<uint64_t> t((size_t)(s * s));
+    bool uniform = true;
+    uint64_t par[2] = {0, 0};
+    bool have[2] = {false, false}, parity_ok = true;
+    for (int64_t r = 0; r < s; ++r)
+        for (int64_t c = 0; c < s; ++c) {
+            const uint64_t v = threshold_of(p_up[r * s + c]);
+            t[(size_t)(r * s + c)] = v;
+            if (v != t[0]) uniform = false;
+            const int p = (int)((r + c) & 1);
+            if (!have[p]) { have[p] = true; par[p] = v; }
+            else if (par[p] != v) parity_ok = false;
+        }
+    if (uniform) {
+        h->tmode = 0;
+        h->t0 = h->t1 = t[0];
+    } else if (parity_ok) {
+        h->tmode = 1;
+        h->t0 = par[0];
+        h->t1 = par[1];
+    } else {
+        h->tmode = 2;
+        if (!h->tgrid) TSB_CUDA(cudaMalloc(&h->tgrid, sizeof(uint64_t) * t.size()));
+        TSB_CUDA(cudaMemcpyAsync(h->tgrid, t.data(), sizeof(uint64_t) * t.size(), cudaMemcpyHostToDevice,
+                                 h->stream));
+        TSB_CUDA(cudaStreamSynchronize(h->stream));
+    }
+    return TSB_OK;
+}
+
+int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states) {
+    int rc = check_range(h, chain0, n);
+    if (rc || n == 0) return rc;
+    TSB_CUDA(cudaSetDevice(h->device));
+    const size_t grid = (size_t)h->side * h->side;
+    if ((rc = ensure_bytes(h, grid * n))) return rc;
+    TSB_CUDA(cudaMemcpyAsync(h->bytes, states, grid * n, cudaMemcpyHostToDevice, h->stream));
+    TSB_CUDA(cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
+    pack_kernel<<<dim3((h->W + 127) / 128, h->side, n), 128, 0, h->stream>>>(
+        h->bytes, h->side, h->W, h->pitch, h->chain_stride, h->dom,
+        h->buf[h->cur] + (size_t)chain0 * h->chain_stride, h->bad);
+    TSB_CUDA(cudaGetLastError());
+    int bad = 0;
+    TSB_CUDA(cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (bad & 1) return fail(TSB_E_INCONSISTENT, "tilestate values must be < 16");
+    if (bad & 2) return fail(TSB_E_INCONSISTENT, "edge bit not mirrored by the neighbouring vertex");
+    if (bad & 4) return fail(TSB_E_INCONSISTENT, "crossed edge leaves the grid or the domain");
+    return TSB_OK;
+}
+
+int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states) {
+    int rc = check_range(h, chain0, n);
+    if (rc || n == 0) return rc;
+    TSB_CUDA(cudaSetDevice(h->device));
+    const size_t grid = (size_t)h->side * h->side;
+    if ((rc = ensure_bytes(h, grid * n))) return rc;
+    unpack_kernel<<<dim3((h->side + 127) / 128, h->side, n), 128, 0, h->stream>>>(
+        h->buf[h->cur] + (size_t)chain0 * h->chain_stride, h->side, h->pitch, h->chain_stride, h->bytes);
+    TSB_CUDA(cudaGetLastError());
+    TSB_CUDA(cudaMemcpyAsync(states, h->bytes, grid * n, cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    return TSB_OK;
+}
+
+int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step0,
+                    uint64_t n_steps) {
+    int rc = check_range(h, chain0, n);
+    if (rc || n == 0 || n_steps == 0) return rc;
+    if (!seeds) return fail(TSB_E_VALUE, "null seeds");
+    TSB_CUDA(cudaSetDevice(h->device));
+    if ((rc = push_seeds(h, n, seeds))) return rc;
+    for (uint64_t s = 0; s < n_steps; ++s)
+        if ((rc = launch_sweep(h, chain0, n, step0 + s, -1))) return rc;
+    return settle(h, chain0, n, n_steps);
+}
+
+int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int color) {
+    int rc = check_range(h, chain0, n);
+    if (rc || n == 0) return rc;
+    if (color != 0 && color != 1) return fail(TSB_E_VALUE, "colour must be 0 (BLACK) or 1 (WHITE)");
+    TSB_CUDA(cudaSetDevice(h->device));
+    if ((rc = push_seeds(h, n, seeds))) return rc;
+    if ((rc = launch_sweep(h, chain0, n, step, color))) return rc;
+    return settle(h, chain0, n, 1);
+}
+
+int tsb_domino_sync(tsb_domino *h) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    TSB_CUDA(cudaSetDevice(h->device));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    return TSB_OK;
+}
+
+int tsb_domino_walk_host(int device, uint8_t *states, int nchains, int side, const uint64_t *seeds,
+                         const double *p_up, const uint8_t *faces, uint64_t n_steps) {
+    tsb_domino *h = nullptr;
+    int rc = tsb_domino_create(device, side, nchains, faces, &h);
+    if (rc) return rc;
+    if (!rc && p_up) rc = tsb_domino_set_p_up(h, p_up);
+    if (!rc) rc = tsb_domino_upload(h, 0, nchains, states);
+    if (!rc) rc = tsb_domino_walk(h, 0, nchains, seeds, 0, n_steps);
+    if (!rc) rc = tsb_domino_download(h, 0, nchains, states);
+    tsb_domino_destroy(h);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// Domino handle shared by the domino translation units.
+#pragma once
+
+#include "tsb_internal.cuh"
+
+struct tsb_domino {
+    int device = 0, side = 0, nchains = 0, W = 0, pitch = 0;
+    size_t chain_stride = 0;  // uint2 elements per chain
+    uint2 *buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    uint4 *dom = nullptr;        // {crossable V, crossable H, existing V, existing H} per word
+    uint32_t *fbits = nullptr;   // face (r, c) in the domain
+    int2 *range = nullptr;
+    int tmode = 0;
+    uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
+    uint64_t *tgrid = nullptr;
+    uint64_t *seedinfo = nullptr;  // device [nchains][2]
+    uint64_t *seed_pinned = nullptr;
+    cudaEvent_t seed_ev = nullptr;
+    uint8_t *bytes = nullptr;  // device staging for tilestate grids
+    size_t bytes_cap = 0;
+    int *bad = nullptr;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+};
+
+
+namespace tsb {
+int ensure_bytes(tsb_domino *h, size_t need);
+int check_range(tsb_domino *h, int chain0, int n);
+int push_seeds(tsb_domino *h, int n, const uint64_t *seeds);
+int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override);
+int settle(tsb_domino *h, int chain0, int n, uint64_t nsweeps);
+}  // namespace tsb

@@ -1,0 +1,362 @@
+"""Cluster Glauber dynamics for domino tilings -- device-backed.
+
+Drop-in mirror of the reference's `sweeps.py` (same names, signatures and
+results, sweeps.py:1-362).  Every sweep runs in the sm_100a kernel
+`domino_sweep_kernel` (csrc/domino.cu) through the C ABI; the `backend`
+argument is accepted for signature compatibility and ignored (the device is
+the backend).  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from collections import OrderedDict
+from dataclasses import dataclass, field
+from functools import cached_property
+
+import numpy as np
+
+from . import _native, rng
+from .lattice import (
+    HORIZONTAL_PAIR,
+    VERTICAL_PAIR,
+    Domain,
+    EdgeWeights,
+    Tiling,
+    Uniform,
+    VolumeWeights,
+    WeightSpec,
+    rotation_height_delta,
+)
+
+
+class Color(enum.IntEnum):
+    """Checkerboard vertex colours; BLACK is even coordinate sum (sweeps.py:40-44)."""
+
+    BLACK = 0
+    WHITE = 1
+
+
+class Sequential:
+    """Signature-compatible stand-in for the reference's CPU band executor
+    (sweeps.py:47-56).  The device runs every sweep; no CPU bands exist."""
+
+    workers = 1
+
+    def run_bands(self, n_rows: int, fn) -> None:
+        fn(0, n_rows)
+
+    def __repr__(self):
+        return "Sequential()"
+
+
+class MultiThreaded(Sequential):
+    """Signature-compatible stand-in for the reference's threaded backend
+    (sweeps.py:59-93); results are identical by construction."""
+
+    def __init__(self, workers: int):
+        if workers < 1:
+            raise ValueError("worker count must be positive")
+        self.workers = workers
+
+    def __repr__(self):
+        return f"MultiThreaded({self.workers})"
+
+
+Backend = Sequential | MultiThreaded
+
+
+def rotate_kernel(s: int, u: float, p_up: float) -> int:
+    """Scalar rotate semantics (sweeps.py:102-110)."""
+    if u < p_up:
+        return VERTICAL_PAIR if s == HORIZONTAL_PAIR else s
+    return HORIZONTAL_PAIR if s == VERTICAL_PAIR else s
+
+
+def update_kernel(t_self: np.ndarray, t_other: np.ndarray, i: int, j: int, color: Color) -> int:
+    """Scalar update semantics on checkerboard sub-arrays (sweeps.py:113-131)."""
+    par = i % 2 if color == Color.BLACK else (i + 1) % 2
+
+    def other(a: int, b: int) -> int:
+        if 0 <= a < t_other.shape[0] and 0 <= b < t_other.shape[1]:
+            return int(t_other[a, b])
+        return 0
+
+    return (
+        ((other(i - 1, j) & 2) >> 1)
+        | ((other(i + 1, j) & 1) << 1)
+        | ((other(i, j + par - 1) & 8) >> 1)
+        | ((other(i, j + par) & 4) << 1)
+    )
+
+
+def heat_bath_p_up(vertex: tuple[int, int], w: WeightSpec) -> float:
+    """W_up / (W_up + W_down) at one vertex (sweeps.py:134-150)."""
+    if isinstance(w, Uniform):
+        return 0.5
+    if isinstance(w, VolumeWeights):
+        ratio = w.q(vertex) ** rotation_height_delta(vertex)
+        return ratio / (1.0 + ratio)
+    if isinstance(w, EdgeWeights):
+        r, c = vertex
+        w_up = w.weight((r - 1, c - 1), (r, c - 1)) * w.weight((r - 1, c), (r, c))
+        w_down = w.weight((r - 1, c - 1), (r - 1, c)) * w.weight((r, c - 1), (r, c))
+        return w_up / (w_up + w_down)
+    raise TypeError(f"unsupported weight spec {type(w)!r}")
+
+
+def _p_up_grid(v: int, w: WeightSpec) -> np.ndarray:
+    """Vectorised SweepPlan.p_up, bit-identical to the per-vertex loop
+    (sweeps.py:170-179): powers are taken with Python floats on the few
+    distinct q values, products/quotients are IEEE-exact in numpy too."""
+    if isinstance(w, Uniform):
+        return np.full((v, v), 0.5)
+    if isinstance(w, VolumeWeights):
+        par = (np.arange(v)[:, None] + np.arange(v)[None, :]) % 2
+        grid = np.empty((v, v))
+        for p in (0, 1):
+            ratio = w.default ** (4 if p == 0 else -4)
+            grid[par == p] = ratio / (1.0 + ratio)
+        for (r, c) in w.overrides:
+            if 0 <= r < v and 0 <= c < v:
+                grid[r, c] = heat_bath_p_up((r, c), w)
+        return grid
+    if isinstance(w, EdgeWeights):
+        d = float(w.default)
+        a = np.full((v, v), d)  # w((r-1,c-1),(r,c-1))
+        b = np.full((v, v), d)  # w((r-1,c),(r,c))
+        c_ = np.full((v, v), d)  # w((r-1,c-1),(r-1,c))
+        e = np.full((v, v), d)  # w((r,c-1),(r,c))
+        touched = []
+        for key, val in w.overrides.items():
+            fa, fb = sorted(key)
+            (ra, ca), (rb, cb) = fa, fb
+            if ca == cb and rb == ra + 1:  # vertical face pair
+                for (rr, cc, arr) in ((rb, ca + 1, a), (rb, ca, b)):
+                    if 0 <= rr < v and 0 <= cc < v:
+                        arr[rr, cc] = val
+                        touched.append((rr, cc))
+            elif ra == rb and cb == ca + 1:  # horizontal face pair
+                for (rr, cc, arr) in ((ra + 1, cb, c_), (ra, cb, e)):
+                    if 0 <= rr < v and 0 <= cc < v:
+                        arr[rr, cc] = val
+                        touched.append((rr, cc))
+        w_up = a * b
+        w_dn = c_ * e
+        return w_up / (w_up + w_dn)
+    raise TypeError(f"unsupported weight spec {type(w)!r}")
+
+
+@dataclass(frozen=True)
+class SweepPlan:
+    """Frozen per-domain sweep data: colour classes and flip probabilities
+    (sweeps.py:153-179)."""
+
+    domain: Domain
+    weights: WeightSpec = field(default_factory=Uniform)
+
+    @cached_property
+    def parity(self) -> np.ndarray:
+        v = self.domain.n + 1
+        r = np.arange(v)
+        return ((r[:, None] + r[None, :]) % 2).astype(np.uint8)
+
+    def color_class(self, color: Color) -> np.ndarray:
+        return self.parity == int(color)
+
+    @cached_property
+    def p_up(self) -> np.ndarray:
+        return _p_up_grid(self.domain.n + 1, self.weights)
+
+
+# -- device handles ------------------------------------------------------------
+
+
+class DominoHandle:
+    """Owns a batch of device-resident domino chains (tsb_domino)."""
+
+    def __init__(self, domain: Domain | None, side: int, nchains: int, device: int | None = None):
+        L = _native.lib()
+        self.side = side
+        self.nchains = nchains
+        self.device = _native.device() if device is None else device
+        self.domain = domain
+        self._p_up_id = None
+        self._p_up_ref = None
+        self._h = ctypes.c_void_p()
+        faces = domain.faces_u8 if domain is not None else None
+        _native.check(L.tsb_domino_create(self.device, side, nchains,
+                                          None if faces is None else _native.ptr(faces),
+                                          ctypes.byref(self._h)))
+
+    def __del__(self):
+        try:
+            if self._h:
+                _native.lib().tsb_domino_destroy(self._h)
+                self._h = ctypes.c_void_p()
+        except Exception:  # interpreter shutdown
+            pass
+
+    def set_stream(self, stream_ptr: int):
+        _native.check(_native.lib().tsb_domino_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    def set_p_up(self, p_up: np.ndarray):
+        if self._p_up_ref is p_up:
+            return
+        p = np.ascontiguousarray(p_up, dtype=np.float64)
+        if p.shape != (self.side, self.side):
+            raise ValueError(f"p_up must be {(self.side, self.side)}")
+        _native.check(_native.lib().tsb_domino_set_p_up(self._h, _native.ptr(p)))
+        self._p_up_ref = p_up
+
+    def upload(self, states: np.ndarray, chain0: int = 0):
+        s = np.ascontiguousarray(states, dtype=np.uint8)
+        _native.check(_native.lib().tsb_domino_upload(self._h, chain0, s.shape[0], _native.ptr(s)))
+
+    def download(self, chain0: int = 0, n: int | None = None) -> np.ndarray:
+        n = self.nchains - chain0 if n is None else n
+        out = np.empty((n, self.side, self.side), dtype=np.uint8)
+        _native.check(_native.lib().tsb_domino_download(self._h, chain0, n, _native.ptr(out)))
+        return out
+
+    def walk(self, seeds, n_steps: int, step0: int = 0, chain0: int = 0):
+        s = np.ascontiguousarray(seeds, dtype=np.uint64)
+        _native.check(_native.lib().tsb_domino_walk(self._h, chain0, s.shape[0], _native.ptr(s),
+                                                    _native.u64(step0), int(n_steps)))
+
+    def sweep(self, seeds, step: int, color: int, chain0: int = 0):
+        s = np.ascontiguousarray(seeds, dtype=np.uint64)
+        _native.check(_native.lib().tsb_domino_sweep(self._h, chain0, s.shape[0], _native.ptr(s),
+                                                     _native.u64(step), int(color)))
+
+    def sync(self):
+        _native.check(_native.lib().tsb_domino_sync(self._h))
+
+    def heights(self, chain: int, ref) -> np.ndarray:
+        out = np.empty((self.side, self.side), dtype=np.int32)
+        _native.check(_native.lib().tsb_domino_heights(self._h, chain, int(ref[0]), int(ref[1]),
+                                                       _native.ptr(out)))
+        return out
+
+    def extremal(self, ref, chain_max: int = 0, chain_min: int = 1) -> bool:
+        rc = _native.lib().tsb_domino_extremal(self._h, chain_max, chain_min, int(ref[0]), int(ref[1]))
+        if rc == _native.E_UNTILEABLE:
+            return False
+        _native.check(rc)
+        return True
+
+
+_CACHE: "OrderedDict[tuple, DominoHandle]" = OrderedDict()
+_CACHE_MAX = 8
+
+
+def _handle_for(domain: Domain | None, nchains: int, side: int | None = None) -> DominoHandle:
+    side = domain.n + 1 if domain is not None else side
+    key = (domain._key if domain is not None else None, side, nchains, _native.device())
+    h = _CACHE.get(key)
+    if h is None:
+        h = DominoHandle(domain, side, nchains)
+        _CACHE[key] = h
+        while len(_CACHE) > _CACHE_MAX:
+            _CACHE.popitem(last=False)
+    else:
+        _CACHE.move_to_end(key)
+    return h
+
+
+def random_walk_batch(
+    states: np.ndarray,
+    seeds: np.ndarray,
+    n_steps: int,
+    plan: SweepPlan,
+    backend: Backend | None = None,
+    use_fused: bool | None = None,
+) -> np.ndarray:
+    """Evolve a (B, V, V) batch for n_steps coupled cluster sweeps on the
+    device (sweeps.py:278-316).  Chain b's result depends on seeds[b] only."""
+    states = np.asarray(states)
+    v = states.shape[-1]
+    seeds = np.asarray(seeds, dtype=np.uint64)
+    out = states.astype(np.uint8, copy=True)
+    if n_steps <= 0 or out.shape[0] == 0:
+        return out
+    h = _handle_for(plan.domain, out.shape[0]) if plan.domain.n + 1 == v else _handle_for(None, out.shape[0], v)
+    h.set_p_up(plan.p_up)
+    h.upload(out)
+    h.walk(seeds, n_steps)
+    return h.download()
+
+
+def sweep(
+    t: Tiling,
+    f: rng.StreamFamily,
+    step: int,
+    color: Color,
+    plan: SweepPlan,
+    backend: Backend | None = None,
+    return_rotated: bool = False,
+):
+    """One sweep of `color` at `step` with family f's coins (sweeps.py:322-342)."""
+    h = _handle_for(plan.domain, 1)
+    h.set_p_up(plan.p_up)
+    h.upload(t.states[None])
+    h.sweep([f.seed], step, int(color))
+    new = h.download()[0]
+    result = Tiling(t.domain, new)
+    if return_rotated:
+        rotated = (new != t.states) & plan.color_class(color)
+        return result, rotated
+    return result
+
+
+def random_walk(
+    t: Tiling,
+    seed: int,
+    n_steps: int,
+    plan: SweepPlan,
+    backend: Backend | None = None,
+) -> Tiling:
+    """n_steps sweeps with the colour chosen per step (sweeps.py:345-362)."""
+    if n_steps < 0:
+        raise ValueError("step count must be non-negative")
+    states = random_walk_batch(t.states[None, :, :], np.array([seed], dtype=np.uint64), n_steps, plan, backend)
+    return Tiling(t.domain, states[0])
+
+
+class DominoCftp:
+    """Device CFTP runner for a batch of samples (csrc/cftp.cu, tsb_domino_cftp)."""
+
+    def __init__(self, domain: Domain, plan: SweepPlan, top0: np.ndarray, bot0: np.ndarray, count: int):
+        self.domain = domain
+        self.count = count
+        self.top0 = np.ascontiguousarray(top0, dtype=np.uint8)
+        self.bot0 = np.ascontiguousarray(bot0, dtype=np.uint8)
+        self.handle = _handle_for(domain, 2 * count + 2)
+        self.handle.set_p_up(plan.p_up)
+
+    def run(self, masters, max_doublings: int, progress=None, trace=None) -> np.ndarray:
+        masters = np.ascontiguousarray(masters, dtype=np.uint64)
+        b = len(masters)
+        v = self.domain.n + 1
+        out = np.zeros((b, v, v), dtype=np.uint8)
+        rounds = np.zeros(b, dtype=np.int32)
+        cb = None
+        if progress is not None:
+            cb = _native.PROGRESS_FN(lambda r, s, c, t, u: progress(r, int(s), c, t))
+        rc = _native.lib().tsb_domino_cftp(
+            self.handle._h, _native.ptr(self.top0), _native.ptr(self.bot0), _native.ptr(masters), b,
+            int(max_doublings), _native.ptr(out), _native.ptr(rounds),
+            ctypes.cast(cb, ctypes.c_void_p) if cb is not None else None, None)
+        if trace is not None and b > 0:
+            from .cftp import schedule_seed
+
+            last = int(rounds[0]) if rc == _native.OK else int(max_doublings)
+            m0 = int(masters[0])
+            seeds = [schedule_seed(m0, i) for i in range(1, last + 1)]
+            for r in range(1, last + 1):
+                trace.rounds.append([(seeds[i - 1], 2**i) for i in range(r, 0, -1)])
+            if rc == _native.OK:
+                trace.collapsed_at = last
+        _native.check(rc)
+        return out

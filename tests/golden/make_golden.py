@@ -84,7 +84,7 @@ def make_domino():
 
     arrays = {}
     for i, case in enumerate(gc.domino_walk_cases()):
-        d, plan, start = case["domain"], case["plan"], case["start"]
+        d, plan, start = case["domain"], case["plan"], case["start"]()
         states = np.stack(start)
         seeds = np.asarray(case["seeds"], dtype=np.uint64)
         res = ts.random_walk_batch(states, seeds, case["n_steps"], plan)

@@ -61,6 +61,19 @@ def random_tileable_domain(ts, rng: np.random.Generator, n: int):
             return d
 
 
+def _both(ts, d):
+    ext = ts.extremal_tilings(d)
+    return [ext[0].states, ext[1].states]
+
+
+def domino_walk_weights(ts):
+    """Weight spec of each domino_walk_cases entry, in order."""
+    return ([ts.VolumeWeights(1.0, {(2, 3): 2.0})] + [ts.Uniform()] * 6
+            + [ts.EdgeWeights(1.0, {((3, 4), (3, 5)): 3.0, ((7, 7), (8, 7)): 0.25, ((0, 0), (0, 1)): 5.0}),
+               ts.VolumeWeights(0.9), ts.Uniform(), ts.Uniform(),
+               ts.VolumeWeights(1.05, {(40, 40): 3.0, (10, 40): 0.5})])
+
+
 def domino_walk_cases(ts=None):
     if ts is None:
         import tilesampler as ts  # reference, only when generating
@@ -68,36 +81,29 @@ def domino_walk_cases(ts=None):
     # sweeps.py fused==numpy test (tests/test_sweeps.py:160-168)
     d = ts.Domain.aztec(3)
     plan = ts.SweepPlan(d, ts.VolumeWeights(1.0, {(2, 3): 2.0}))
-    t0 = ts.extremal_tilings(d)[1]
-    cases.append(dict(domain=d, plan=plan, start=[t0.states] * 5,
+    cases.append(dict(domain=d, plan=plan, start=lambda d=d: [ts.extremal_tilings(d)[1].states] * 5,
                       seeds=list(range(11, 16)), n_steps=97))
     rng = np.random.default_rng(2024)
     for k in range(6):
         d = random_tileable_domain(ts, rng, 12)
-        ext = ts.extremal_tilings(d)
-        cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=[ext[0].states, ext[1].states],
+        cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=lambda d=d: _both(ts, d),
                           seeds=[1000 + k, 2000 + k], n_steps=150 + 7 * k))
     d = ts.Domain.square(16)
     w = ts.EdgeWeights(1.0, {((3, 4), (3, 5)): 3.0, ((7, 7), (8, 7)): 0.25, ((0, 0), (0, 1)): 5.0})
-    ext = ts.extremal_tilings(d)
-    cases.append(dict(domain=d, plan=ts.SweepPlan(d, w), start=[ext[0].states, ext[1].states],
+    cases.append(dict(domain=d, plan=ts.SweepPlan(d, w), start=lambda d=d: _both(ts, d),
                       seeds=[3, 2**63 + 9], n_steps=150))
     d = ts.Domain.aztec(20)
-    ext = ts.extremal_tilings(d)
     cases.append(dict(domain=d, plan=ts.SweepPlan(d, ts.VolumeWeights(0.9)),
-                      start=[ext[0].states], seeds=[0x5EED], n_steps=300))
+                      start=lambda d=d: _both(ts, d)[:1], seeds=[0x5EED], n_steps=300))
     d = ts.Domain.rectangle(2, 3)
-    ext = ts.extremal_tilings(d)
-    cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=[ext[0].states] * 3,
+    cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=lambda d=d: _both(ts, d)[:1] * 3,
                       seeds=[5, 6, 7], n_steps=40))
     d = ts.Domain.rectangle(30, 70)  # non-square box, wide rows (> 64 columns)
-    ext = ts.extremal_tilings(d)
-    cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=[ext[1].states],
+    cases.append(dict(domain=d, plan=ts.SweepPlan(d), start=lambda d=d: _both(ts, d)[1:],
                       seeds=[99], n_steps=211))
     d = ts.Domain.aztec(40)
-    ext = ts.extremal_tilings(d)
     w = ts.VolumeWeights(1.05, {(40, 40): 3.0, (10, 40): 0.5})
-    cases.append(dict(domain=d, plan=ts.SweepPlan(d, w), start=[ext[0].states, ext[1].states],
+    cases.append(dict(domain=d, plan=ts.SweepPlan(d, w), start=lambda d=d: _both(ts, d),
                       seeds=[17, 18], n_steps=257))
     return cases
 

@@ -1,0 +1,207 @@
+"""Domino parity on the device: the CUDA path vs the reference's golden
+outputs and vs the C oracle (bit-exact; integer/byte work)."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import oracle
+import paper_1804_07250_b200 as ts
+from paper_1804_07250_b200.sweeps import DominoHandle
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(G, name))
+
+
+def fp(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def dom(faces):
+    return ts.Domain(faces.shape[0], faces)
+
+
+def test_c1_fingerprint():
+    """BASELINE config 1: Aztec 64, T_max, seed 0x5EED, 1000 sweeps."""
+    g = load("domino_c1.npz")
+    d = ts.Domain.aztec(64)
+    t = ts.random_walk(ts.Tiling(d, g["t_max"]), 0x5EED, 1000, ts.SweepPlan(d))
+    assert fp(t.states) == "fe33268e95b1a840"
+    assert np.array_equal(t.states, g["final"])
+
+
+def test_golden_walk_cases():
+    g = load("domino_walks.npz")
+    for i, w in enumerate(gc.domino_walk_weights(ts)):
+        d = dom(g[f"c{i}_faces"])
+        plan = ts.SweepPlan(d, w)
+        out = ts.random_walk_batch(g[f"c{i}_start"], g[f"c{i}_seeds"], int(g[f"c{i}_n_steps"]), plan)
+        assert np.array_equal(out, g[f"c{i}_out"]), f"case {i}"
+
+
+def test_golden_single_sweeps():
+    g = load("domino_walks.npz")
+    for j, (_, seed, step, color) in enumerate(gc.SWEEP_CASES):
+        d = dom(g[f"s{j}_faces"])
+        t0 = ts.Tiling(d, g[f"s{j}_in"])
+        fam = ts.seed_family(seed, (d.n + 1, d.n + 1))
+        t1, rot = ts.sweep(t0, fam, step, ts.Color(color), ts.SweepPlan(d), return_rotated=True)
+        assert np.array_equal(t1.states, g[f"s{j}_out"])
+        assert np.array_equal(rot, g[f"s{j}_rot"])
+
+
+def test_uniform_grid_device():
+    g = load("rng_grids.npz")
+    for name in g.files:
+        seed, r, c, step = (int(x) for x in name.split("_"))
+        assert np.array_equal(ts.seed_family(seed, (r, c)).uniform_grid(step), g[name])
+
+
+@pytest.mark.parametrize("order,steps,seed", [(50, 400, 1), (97, 333, 2**63 + 5), (130, 257, 0x5EED)])
+def test_walk_vs_oracle_aztec(order, steps, seed):
+    """Seeded parity vs the C oracle beyond the golden sizes (odd orders give
+    side % 32 != 0, several warps per row and partially covered words)."""
+    g = load("domino_c1.npz")
+    d = ts.Domain.aztec(order)
+    ext = ts.extremal_tilings(d)
+    plan = ts.SweepPlan(d)
+    start = np.stack([ext[0].states, ext[1].states])
+    seeds = np.array([seed, seed + 1], dtype=np.uint64)
+    out = ts.random_walk_batch(start, seeds, steps, plan)
+    ref = oracle.domino_walk(start, seeds, plan.p_up, steps, threads=4)
+    assert np.array_equal(out, ref)
+
+
+def test_walk_vs_oracle_weighted_square():
+    d = ts.Domain.square(70)
+    w = ts.VolumeWeights(0.8, {(5, 5): 3.0, (69, 1): 0.1})
+    plan = ts.SweepPlan(d, w)
+    ext = ts.extremal_tilings(d)
+    start = np.stack([ext[1].states])
+    out = ts.random_walk_batch(start, [12345], 500, plan)
+    assert np.array_equal(out, oracle.domino_walk(start, [12345], plan.p_up, 500))
+
+
+def test_split_walk_equals_one_walk():
+    d = ts.Domain.aztec(40)
+    plan = ts.SweepPlan(d)
+    ext = ts.extremal_tilings(d)
+    h = DominoHandle(d, d.n + 1, 2)
+    h.set_p_up(plan.p_up)
+    start = np.stack([ext[0].states, ext[1].states])
+    h.upload(start)
+    h.walk([7, 8], 37)
+    h.walk([7, 8], 100, step0=37)
+    a = h.download()
+    b = ts.random_walk_batch(start, [7, 8], 137, plan)
+    assert np.array_equal(a, b)
+    # subset walks keep the other chain untouched
+    h.upload(start)
+    h.walk([9], 11, chain0=1)
+    c = h.download()
+    assert np.array_equal(c[0], start[0])
+    assert np.array_equal(c[1], ts.random_walk_batch(start[1:], [9], 11, plan)[0])
+
+
+def test_batch_matches_single_chain_runs():
+    d = ts.Domain.rectangle(2, 3)
+    plan = ts.SweepPlan(d)
+    t0 = ts.extremal_tilings(d)[0]
+    seeds = np.array([5, 6, 7], dtype=np.uint64)
+    batch = ts.random_walk_batch(np.repeat(t0.states[None], 3, axis=0), seeds, 40, plan)
+    for i, s in enumerate(seeds):
+        assert np.array_equal(batch[i], ts.random_walk(t0, int(s), 40, plan).states)
+
+
+def test_zero_steps_and_errors():
+    d = ts.Domain.rectangle(2, 3)
+    plan = ts.SweepPlan(d)
+    t0 = ts.extremal_tilings(d)[0]
+    assert ts.random_walk(t0, 7, 0, plan) == t0
+    with pytest.raises(ValueError):
+        ts.random_walk(t0, 7, -1, plan)
+    bad = t0.states.copy()
+    bad[0, 0] ^= 2  # unmirrored edge bit
+    with pytest.raises(ts.InconsistencyError):
+        ts.random_walk_batch(bad[None], [1], 3, plan)
+    bad = t0.states.copy()
+    bad[1, 1] = 200
+    with pytest.raises(ts.InconsistencyError):
+        ts.random_walk_batch(bad[None], [1], 3, plan)
+
+
+def test_extremal_and_heights_golden():
+    g = load("domino_extremal.npz")
+    for i, d in enumerate(gc.extremal_domains(ts)):
+        ext = ts.extremal_tilings(d)
+        if f"d{i}_none" in g.files:
+            assert ext is None, f"domain {i} should be untileable"
+            continue
+        assert ext is not None, f"domain {i}"
+        assert np.array_equal(ext[0].states, g[f"d{i}_tmax"]), f"tmax {i}"
+        assert np.array_equal(ext[1].states, g[f"d{i}_tmin"]), f"tmin {i}"
+        for key in ("max", "min", "mixed"):
+            st = g[f"d{i}_t{key}"] if key != "mixed" else g[f"d{i}_mixed"]
+            hf = ts.height_function(ts.Tiling(d, st))
+            assert np.array_equal(hf.heights, g[f"d{i}_h{key}"]), f"heights {key} {i}"
+
+
+def test_c1_heights():
+    g = load("domino_c1.npz")
+    d = ts.Domain.aztec(64)
+    assert np.array_equal(ts.height_function(ts.Tiling(d, g["final"])).heights, g["heights"])
+    assert np.array_equal(ts.height_function(ts.Tiling(d, g["t_max"])).heights, g["heights_tmax"])
+    ext = ts.extremal_tilings(d)
+    assert np.array_equal(ext[0].states, g["t_max"]) and np.array_equal(ext[1].states, g["t_min"])
+
+
+def test_untileable():
+    d = ts.Domain.from_faces(2, [(0, 0), (0, 1), (1, 0)])
+    assert ts.extremal_tilings(d) is None
+    with pytest.raises(ts.UntileableDomain):
+        ts.cftp_sample(d, ts.SweepPlan(d), 1)
+
+
+def test_cftp_golden():
+    g = load("domino_cftp.npz")
+    traces = json.load(open(os.path.join(G, "domino_cftp_traces.json")))
+    weights = [ts.Uniform(), ts.Uniform(), ts.VolumeWeights(1.0, {(2, 3): 2.0}), ts.Uniform(), ts.Uniform()]
+    masters = [999, 3, 271828, 271828, 0x5EED]
+    counts = [7, 3, 4, 1, 2]
+    for i in range(5):
+        d = dom(g[f"k{i}_faces"])
+        trace = ts.CftpTrace()
+        samples = ts.cftp_sample_many(d, ts.SweepPlan(d, weights[i]), masters[i], counts[i], trace=trace)
+        assert np.array_equal(np.stack([s.states for s in samples]), g[f"k{i}_samples"]), f"case {i}"
+        assert [[list(p) for p in r] for r in trace.rounds] == traces[i]["rounds"]
+        assert trace.collapsed_at == traces[i]["collapsed_at"]
+
+
+def test_cftp_batching_and_progress():
+    import io
+
+    d = ts.Domain.rectangle(2, 3)
+    plan = ts.SweepPlan(d)
+    a = ts.cftp_sample_many(d, plan, 999, 7, batch_size=2)
+    b = ts.cftp_sample_many(d, plan, 999, 7, batch_size=7)
+    singles = [ts.cftp_sample_many(d, plan, 999, k + 1)[k] for k in range(7)]
+    assert a == b == singles
+    buf = io.StringIO()
+    ts.cftp_sample(ts.Domain.square(4), ts.SweepPlan(ts.Domain.square(4)), 3, progress=buf)
+    lines = buf.getvalue().strip().splitlines()
+    assert lines[-1].endswith("collapsed=True")
+    assert all(ln.endswith("collapsed=False") for ln in lines[:-1])
+    with pytest.raises(ts.ConvergenceCapExceeded):
+        ts.cftp_sample(ts.Domain.square(6), ts.SweepPlan(ts.Domain.square(6)), 1, max_doublings=2)
+    one = ts.Domain.rectangle(1, 2)
+    trace = ts.CftpTrace()
+    ts.cftp_sample(one, ts.SweepPlan(one), 9, trace=trace)
+    assert trace.rounds == []

@@ -1,0 +1,146 @@
+"""Host-side logic that runs without a GPU: domain construction, p_up grids,
+codecs, seed derivation, and the C-ABI library's exported symbols."""
+
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import paper_1804_07250_b200 as ts
+from paper_1804_07250_b200 import _native, rng
+from paper_1804_07250_b200.cftp import chain_master_seed, schedule_seed
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(G, name))
+
+
+def test_library_exports_every_declared_symbol():
+    path = _native.LIB_PATH
+    if not os.path.exists(path):
+        _native.build()
+    lib = ctypes.CDLL(path)
+    declared = _native.declared_symbols()
+    assert "tsb_domino_walk" in declared and "tsb_domino_cftp" in declared
+    for name in declared:
+        if name == "tsb_progress_fn":
+            continue
+        assert hasattr(lib, name), name
+    assert set(declared) - {"tsb_progress_fn"} <= set(_native._SIGS)
+
+
+def test_no_cpu_fallback_without_device():
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            pytest.skip("device present")
+    except ImportError:
+        pass
+    d = ts.Domain.square(2)
+    with pytest.raises(RuntimeError, match="no CPU fallback|no CUDA device"):
+        ts.random_walk_batch(np.zeros((1, 3, 3), np.uint8), [1], 1, ts.SweepPlan(d))
+
+
+def test_rng_host_scalars_match_kats():
+    kats = json.load(open(os.path.join(G, "rng_kats.json")))
+    for k in kats["kats"]:
+        fam = ts.seed_family(k["seed"], tuple(k["shape"]))
+        assert fam.site_key(tuple(k["site"])) == k["key"]
+        assert fam.uniform(tuple(k["site"]), k["step"]).hex() == k["u"]
+        assert fam.global_uniform(k["step"]).hex() == k["global_u"]
+    for d in kats["derive"]:
+        assert rng.derive_seed(d["seed"], d["index"], d["salt"]) == d["out"]
+    for c in kats["chains"]:
+        assert chain_master_seed(c["master"], c["k"]) == c["chain"]
+        assert schedule_seed(c["chain"], 1) == c["round1"]
+
+
+def test_color_at_matches_global_uniform():
+    fam = ts.seed_family(0x5EED, (5, 5))
+    for step in range(50):
+        assert rng.color_at(0x5EED, step) == (1 if fam.global_uniform(step) >= 0.5 else 0)
+
+
+def test_domains_match_reference_faces():
+    g = load("domino_extremal.npz")
+    doms = gc.extremal_domains(ts)
+    for i, d in enumerate(doms):
+        assert np.array_equal(d.faces, g[f"d{i}_faces"])
+        if f"d{i}_vmask" in g.files:
+            assert np.array_equal(d.vertex_mask, g[f"d{i}_vmask"])
+            assert tuple(g[f"d{i}_ref"]) == d.reference_vertex
+
+
+def test_domain_errors():
+    with pytest.raises(ts.DomainError):
+        ts.Domain.from_faces(3, [(0, 0), (2, 2)])  # disconnected
+    ring = np.ones((3, 3), bool)
+    ring[1, 1] = False
+    with pytest.raises(ts.DomainError):
+        ts.Domain(3, ring)  # hole
+    with pytest.raises(ts.DomainError):
+        ts.Domain(2, np.zeros((2, 2), bool))
+    with pytest.raises(ts.DomainError):
+        ts.Domain.from_faces(2, [(5, 5)])
+    d = ts.Domain.from_text(ts.Domain.aztec(3).to_text())
+    assert d == ts.Domain.aztec(3)
+
+
+def test_p_up_grids_match_reference():
+    g = load("domino_walks.npz")
+    for i, w in enumerate(gc.domino_walk_weights(ts)):
+        f = g[f"c{i}_faces"]
+        plan = ts.SweepPlan(ts.Domain(f.shape[0], f), w)
+        assert np.array_equal(plan.p_up, g[f"c{i}_p_up"]), f"case {i}"
+    assert f"c{i + 1}_p_up" not in g.files
+    # scalar helper
+    assert ts.heat_bath_p_up((1, 1), ts.VolumeWeights(1.0, {(1, 1): 2.0})) == pytest.approx(16 / 17)
+    assert ts.heat_bath_p_up((1, 2), ts.VolumeWeights(1.0, {(1, 2): 2.0})) == pytest.approx(1 / 17)
+
+
+def test_codec_roundtrip_on_golden_tilings():
+    g = load("domino_extremal.npz")
+    for i, d in enumerate(gc.extremal_domains(ts)):
+        if f"d{i}_none" in g.files:
+            continue
+        for key in ("tmax", "tmin", "mixed"):
+            t = ts.Tiling(d, g[f"d{i}_{key}"])
+            pairs = ts.dominoes_from_tiling(t)
+            assert ts.tiling_from_dominoes(d, pairs) == t
+            assert ts.is_valid_tiling(t)
+        # decode heights -> tiling (lattice.py:598-620)
+        assert ts.tiling_from_heights(d, g[f"d{i}_hmax"]).states.tobytes() == g[f"d{i}_tmax"].tobytes()
+        assert ts.tiling_from_heights(d, g[f"d{i}_hmin"]).states.tobytes() == g[f"d{i}_tmin"].tobytes()
+
+
+def test_split_merge_checkerboard():
+    g = load("domino_c1.npz")
+    tb, tw = ts.split_checkerboard(g["final"])
+    merged = ts.merge_checkerboard(tb, tw)
+    assert np.array_equal(merged[:129, :129], g["final"])
+
+
+def test_rotate_kernel_cases():
+    assert ts.rotate_kernel(3, 0.1, 0.5) == 12
+    assert ts.rotate_kernel(12, 0.9, 0.5) == 3
+    assert ts.rotate_kernel(5, 0.1, 0.5) == 5
+
+
+def test_cftp_schedule_prepends():
+    sched = ts.CftpSchedule(master_seed=42, max_doublings=5)
+    seen = []
+    for _ in range(4):
+        sched.grow()
+        seen.append(list(sched.pairs))
+    for earlier, later in zip(seen, seen[1:]):
+        assert later[1:] == earlier
+    assert [s for _, s in sched.pairs] == [16, 8, 4, 2]
+    with pytest.raises(ts.ConvergenceCapExceeded):
+        sched.grow()
+        sched.grow()
