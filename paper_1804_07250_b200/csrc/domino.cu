@@ -30,8 +30,8 @@
 
 namespace tsb {
 
-constexpr int kBand = 16;          // rows marched by one warp
-constexpr int kWarpsPerBlock = 4;  // warps per block (stacked bands)
+constexpr int kTileRows = 15;   // output rows per block tile (+1 halo fire row)
+constexpr int kTileWords = 62;  // output words per tile: 64 loaded (2 per lane), 1 halo word each side
 
 struct SweepCtx {
     const uint2 *src;
@@ -39,6 +39,9 @@ struct SweepCtx {
     const int2 *range;         // [side] word range [lo, hi) that can hold set bits
     const uint64_t *seedinfo;  // [n][2] = {family base, global key}
     const uint64_t *tgrid;     // per-site thresholds (mode 2), (side x side)
+    const uint64_t *step_dev;  // graph replays: step = *step_dev + step (nullable)
+    const int2 *tiles;         // non-empty tiles {word chunk, row band}
+    int ntiles;
     uint64_t t0, t1;           // thresholds for even / odd parity (modes 0, 1)
     size_t chain_stride;       // uint2 per chain (incl. guard rows)
     int side, W, pitch;
@@ -46,133 +49,132 @@ struct SweepCtx {
     int color_override;  // -1: colour from the global coin
 };
 
-// Fire mask of one 32-column word: bit b set iff the active vertex at column
-// 32*w+b is rotateable and its heat-bath coin moves it (3 -> 12 when
-// u < p_up, 12 -> 3 otherwise; _kernels.py:49-55, sweeps.py:102-110).
+// Cold path: draw the heat-bath coin of every rotateable active vertex of a
+// word (bits of `rot`) and return the ones that move: 3 -> 12 when
+// u < p_up, 12 -> 3 otherwise (_kernels.py:49-55, sweeps.py:102-110).  Only
+// rotateable sites pay for the two splitmix64 rounds; counter-based draws
+// make the skipping exact.
 template <int TM>
-__device__ __forceinline__ uint32_t fire_word(uint32_t vu, uint32_t vd, uint32_t h, uint32_t hleft,
-                                              uint32_t act, int r, int w, uint64_t base,
-                                              uint64_t salt, int color, const SweepCtx &c) {
-    const uint32_t l = (h << 1) | (hleft >> 31);
-    const uint32_t is3 = vu & vd & ~(l | h) & act;
-    const uint32_t is12 = ~(vu | vd) & l & h & act;
-    uint32_t rot = is3 | is12;
+__device__ __noinline__ uint32_t rng_fire(uint32_t rot, uint32_t is3, uint64_t row_idx, int w,
+                                          uint64_t base, uint64_t salt, uint64_t t,
+                                          const uint64_t *__restrict__ tgrid) {
     uint32_t fire = 0;
-    while (rot) {
+    do {
         const int b = __ffs(rot) - 1;
         rot &= rot - 1;
-        const uint64_t idx = (uint64_t)r * (uint64_t)c.side + (uint64_t)(w * 32 + b);
+        const uint64_t idx = row_idx + (uint64_t)(w * 32 + b);  // r * side + c
         const uint64_t x = mix64(mix64(base + (idx + 1ull) * kGold) + salt);
-        uint64_t t;
-        if (TM == 0) t = c.t0;
-        else if (TM == 1) t = color ? c.t1 : c.t0;
-        else t = __ldg(c.tgrid + idx);
-        const bool up = (x >> 11) < t;
+        const uint64_t tt = TM == 2 ? __ldg(tgrid + idx) : t;
+        const bool up = (x >> 11) < tt;
         if (up == (bool)((is3 >> b) & 1u)) fire |= 1u << b;
-    }
+    } while (rot);
     return fire;
 }
 
-__device__ __forceinline__ uint2 ld_word(const uint2 *row, int w, int2 rg) {
-    return (w >= rg.x && w < rg.y) ? __ldg(row + w) : make_uint2(0u, 0u);
+// Fire mask of one 32-column word of active vertices.
+template <int TM>
+__device__ __forceinline__ uint32_t fire_mask(uint32_t vu, uint32_t vd, uint32_t h, uint32_t hleft,
+                                              uint32_t act, uint64_t row_idx, int w, uint64_t base,
+                                              uint64_t salt, uint64_t t, const uint64_t *tgrid) {
+    const uint32_t l = (h << 1) | (hleft >> 31);
+    const uint32_t is3 = vu & vd & ~(l | h) & act;
+    const uint32_t is12 = ~(vu | vd) & l & h & act;
+    const uint32_t rot = is3 | is12;
+    return rot ? rng_fire<TM>(rot, is3, row_idx, w, base, salt, t, tgrid) : 0u;
 }
 
-// One sweep.  Warp = 32 consecutive words of one row band; it marches down
-// kBand rows keeping rows r-1, r, r+1 in registers, so every fire row is
-// computed once per band (plus one halo row).  Horizontal neighbours come
-// from lane shuffles; lane 0 / lane 31 fetch the words beyond the warp.
-template <int TM>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    domino_sweep_kernel(SweepCtx c) {
+template <bool COHERENT>
+__device__ __forceinline__ uint4 ld16(const uint2 *p) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4 *>(p)) : __ldg(reinterpret_cast<const uint4 *>(p));
+}
+template <bool COHERENT>
+__device__ __forceinline__ uint2 ld8(const uint2 *p) {
+    return COHERENT ? __ldcg(p) : __ldg(p);
+}
+
+// One tile of one sweep (kTileRows x 62 words, 512 threads).  Warp k owns
+// row r0+k (lane = two adjacent words, 16-byte loads; lanes 0 and 31 hold one
+// halo word each, so horizontal neighbours are shuffles).  Phase 1: every
+// warp computes the fire row F(r) of its row (warp 15 is the halo row r0+15)
+// into shared memory.  Phase 2: warps 0..14 toggle the four incident edges of
+// every firing vertex:
+//   V[r] ^= F(r) ^ F(r+1),   H[r] ^= F(r) ^ F(r) >> 1 (carry from the next word).
+// COHERENT loads (L2 only) are used by the persistent kernel, whose inputs are
+// written by other blocks during the same launch.
+template <int TM, bool COHERENT>
+__device__ __forceinline__ void sweep_tile(const SweepCtx &c, int2 tile, const uint2 *src, uint2 *dst,
+                                           uint64_t base, uint64_t salt, int color, uint2 (*fs)[32]) {
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int w = blockIdx.x * 32 + lane;
-    const int r0 = (blockIdx.y * kWarpsPerBlock + warp) * kBand;
-    if (r0 >= c.side) return;  // warp-uniform
-    const int r1 = min(r0 + kBand, c.side);
-    const int2 *range = c.range;
+    const int k = threadIdx.x >> 5;
+    const int r = tile.y * kTileRows + k;
+    const int wout0 = tile.x * kTileWords - 1;  // first output word of the tile
+    const int wa = wout0 - 1 + 2 * lane, wb = wa + 1;
+    const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
 
-    // Skip warps whose words never hold set bits in this band.
-    {
-        int lo = INT_MAX, hi = INT_MIN;
-        if (lane < r1 - r0) {
-            int2 rg = __ldg(range + r0 + lane);
-            if (rg.y > rg.x) { lo = rg.x; hi = rg.y; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        const int w0 = blockIdx.x * 32;
-        if (hi <= w0 || lo >= w0 + 32) return;  // warp-uniform
+    // rows r-1 (V) and r (V, H); zero outside each row's word range
+    const bool live = r < c.side;
+    const int2 g = live ? __ldg(c.range + r) : make_int2(0, 0);
+    const int2 gm = (live && r > 0) ? __ldg(c.range + r - 1) : make_int2(0, 0);
+    const bool ina = wa >= g.x && wa < g.y, inb = wb >= g.x && wb < g.y;
+    const bool inma = wa >= gm.x && wa < gm.y, inmb = wb >= gm.x && wb < gm.y;
+    const uint2 *row = src + (ptrdiff_t)r * c.pitch;
+    uint4 cur = make_uint4(0u, 0u, 0u, 0u);
+    if (ina && inb) cur = ld16<COHERENT>(row + wa);
+    else {
+        if (ina) { const uint2 x = ld8<COHERENT>(row + wa); cur.x = x.x; cur.y = x.y; }
+        if (inb) { const uint2 x = ld8<COHERENT>(row + wb); cur.z = x.x; cur.w = x.y; }
     }
+    uint32_t vua = 0, vub = 0;
+    if (inma && inmb) { const uint4 q = ld16<COHERENT>(row - c.pitch + wa); vua = q.x; vub = q.z; }
+    else {
+        if (inma) vua = ld8<COHERENT>(row - c.pitch + wa).x;
+        if (inmb) vub = ld8<COHERENT>(row - c.pitch + wb).x;
+    }
+    // lane 0's first word is a pure halo (its fire row feeds no output); lane
+    // 31's second word only feeds bit 0 into the H carry of its first word.
+    const uint32_t act = ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u;
+    const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
+    const uint64_t ridx = (uint64_t)r * (uint64_t)c.side;
+    const uint32_t fa = fire_mask<TM>(vua, cur.x, cur.y, hl, lane == 0 ? 0u : act, ridx, wa, base, salt, t, c.tgrid);
+    const uint32_t fb = fire_mask<TM>(vub, cur.z, cur.w, cur.y, lane == 31 ? act & 1u : act, ridx, wb, base, salt, t,
+                                      c.tgrid);
+    fs[k][lane] = make_uint2(fa, fb);
+    __syncthreads();
+    if (k < kTileRows && live) {  // warp-uniform
+        const uint2 fn = fs[k + 1][lane];  // F(r+1)
+        const uint32_t frb = __shfl_down_sync(0xffffffffu, fa, 1);
+        const uint32_t nva = cur.x ^ fa ^ fn.x;
+        const uint32_t nvb = cur.z ^ fb ^ fn.y;
+        const uint32_t nha = cur.y ^ fa ^ (fa >> 1) ^ (fb << 31);
+        const uint32_t nhb = cur.w ^ fb ^ (fb >> 1) ^ (frb << 31);
+        uint2 *out = dst + (ptrdiff_t)r * c.pitch;
+        const bool sa = lane > 0 && ina, sb = lane < 31 && inb;
+        if (sa && sb) *reinterpret_cast<uint4 *>(out + wa) = make_uint4(nva, nha, nvb, nhb);
+        else {
+            if (sa) out[wa] = make_uint2(nva, nha);
+            if (sb) out[wb] = make_uint2(nvb, nhb);
+        }
+    }
+}
 
+// colour coin: BLACK iff u < 1/2  <=>  bit 63 of the draw is 0
+// (_kernels.py:44-45, sweeps.py:266-269)
+__device__ __forceinline__ int sweep_color(const SweepCtx &c, uint64_t gkey, uint64_t salt) {
+    return c.color_override >= 0 ? c.color_override : (int)(mix64(gkey + salt) >> 63);
+}
+
+// One sweep, one block per non-empty tile.
+template <int TM>
+__global__ void __launch_bounds__(32 * (kTileRows + 1))
+    domino_sweep_kernel(SweepCtx c) {
+    __shared__ uint2 fs[kTileRows + 1][32];
     const int z = blockIdx.z;
-    const uint2 *src = c.src + (size_t)z * c.chain_stride + c.pitch;  // row 0
-    uint2 *dst = c.dst + (size_t)z * c.chain_stride + c.pitch;
+    const uint64_t step = c.step + (c.step_dev ? *c.step_dev : 0ull);
+    const uint64_t salt = (step + 1ull) * kGold;
     const uint64_t base = c.seedinfo[2 * z];
-    const uint64_t gkey = c.seedinfo[2 * z + 1];
-    const uint64_t salt = (c.step + 1ull) * kGold;
-    // colour coin: BLACK iff u < 1/2  <=>  bit 63 of the draw is 0
-    // (_kernels.py:44-45, sweeps.py:266-269)
-    const int color = c.color_override >= 0 ? c.color_override : (int)(mix64(gkey + salt) >> 63);
-    const bool l0 = lane == 0, l31 = lane == 31;
-    const int2 zero2 = make_int2(0, 0);
-
-    auto rg_of = [&](int r) -> int2 { return (r >= 0 && r < c.side) ? __ldg(range + r) : zero2; };
-    auto act_of = [&](int r) -> uint32_t { return ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u; };
-
-    // prologue: row r0-1 (V only) and row r0
-    int2 rgm = rg_of(r0 - 1);
-    int2 rg0 = rg_of(r0);
-    uint32_t vm1 = ld_word(src + (size_t)(r0 - 1) * c.pitch, w, rgm).x;
-    uint2 t = ld_word(src + (size_t)r0 * c.pitch, w, rg0);
-    uint32_t v0 = t.x, h0 = t.y;
-    uint32_t hl = __shfl_up_sync(0xffffffffu, h0, 1);
-    if (l0) hl = ld_word(src + (size_t)r0 * c.pitch, w - 1, rg0).y;
-    // lane 31 also tracks word w+1 (only its bit 0 matters)
-    uint32_t xv0 = 0, xh0 = 0, xvm1 = 0;
-    if (l31) {
-        xvm1 = ld_word(src + (size_t)(r0 - 1) * c.pitch, w + 1, rgm).x;
-        uint2 tx = ld_word(src + (size_t)r0 * c.pitch, w + 1, rg0);
-        xv0 = tx.x;
-        xh0 = tx.y;
-    }
-    uint32_t a0 = act_of(r0);
-    uint32_t f0 = fire_word<TM>(vm1, v0, h0, hl, a0, r0, w, base, salt, color, c);
-    uint32_t fx0 = l31 ? fire_word<TM>(xvm1, xv0, xh0, h0, a0 & 1u, r0, w + 1, base, salt, color, c) : 0u;
-
-    for (int r = r0; r < r1; ++r) {
-        const int2 rgn = rg_of(r + 1);
-        const uint2 *rown = src + (size_t)(r + 1) * c.pitch;
-        uint2 tn = ld_word(rown, w, rgn);
-        const uint32_t v1 = tn.x, h1 = tn.y;
-        uint32_t hl1 = __shfl_up_sync(0xffffffffu, h1, 1);
-        if (l0) hl1 = ld_word(rown, w - 1, rgn).y;
-        uint32_t xv1 = 0, xh1 = 0;
-        if (l31) {
-            uint2 tx = ld_word(rown, w + 1, rgn);
-            xv1 = tx.x;
-            xh1 = tx.y;
-        }
-        const uint32_t a1 = act_of(r + 1);
-        const uint32_t f1 = fire_word<TM>(v0, v1, h1, hl1, a1, r + 1, w, base, salt, color, c);
-        const uint32_t fx1 =
-            l31 ? fire_word<TM>(xv0, xv1, xh1, h1, a1 & 1u, r + 1, w + 1, base, salt, color, c) : 0u;
-        uint32_t fr = __shfl_down_sync(0xffffffffu, f0, 1);
-        if (l31) fr = fx0;
-        const uint32_t nv = v0 ^ f0 ^ f1;
-        const uint32_t nh = h0 ^ f0 ^ (f0 >> 1) ^ (fr << 31);
-        const int2 rgr = rg_of(r);
-        if (w >= rgr.x && w < rgr.y) dst[(size_t)r * c.pitch + w] = make_uint2(nv, nh);
-        v0 = v1;
-        h0 = h1;
-        f0 = f1;
-        xv0 = xv1;
-        xh0 = xh1;
-        fx0 = fx1;
-    }
+    const int color = sweep_color(c, c.seedinfo[2 * z + 1], salt);
+    sweep_tile<TM, false>(c, c.tiles[blockIdx.x], c.src + (size_t)z * c.chain_stride + c.pitch,
+                          c.dst + (size_t)z * c.chain_stride + c.pitch, base, salt, color, fs);
 }
 
 // --------------------------------------------------------------- codecs
@@ -299,8 +301,10 @@ int push_seeds(tsb_domino *h, int n, const uint64_t *seeds) {
     return TSB_OK;
 }
 
-int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override) {
+int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override, cudaStream_t stream,
+                 const uint64_t *step_dev) {
     SweepCtx c;
+    c.step_dev = step_dev;
     c.src = h->buf[h->cur] + (size_t)chain0 * h->chain_stride;
     c.dst = h->buf[h->cur ^ 1] + (size_t)chain0 * h->chain_stride;
     c.range = h->range;
@@ -314,16 +318,61 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     c.pitch = h->pitch;
     c.step = step;
     c.color_override = color_override;
-    const int nbands = (h->side + kBand - 1) / kBand;
-    dim3 grid((h->W + 31) / 32, (nbands + kWarpsPerBlock - 1) / kWarpsPerBlock, n);
-    dim3 block(32 * kWarpsPerBlock);
+    c.tiles = h->tiles;
+    c.ntiles = h->ntiles;
+    if (h->ntiles == 0) { h->cur ^= 1; return TSB_OK; }
+    dim3 grid(h->ntiles, 1, n);
+    dim3 block(32 * (kTileRows + 1));
     switch (h->tmode) {
-        case 0: domino_sweep_kernel<0><<<grid, block, 0, h->stream>>>(c); break;
-        case 1: domino_sweep_kernel<1><<<grid, block, 0, h->stream>>>(c); break;
-        default: domino_sweep_kernel<2><<<grid, block, 0, h->stream>>>(c); break;
+        case 0: domino_sweep_kernel<0><<<grid, block, 0, stream>>>(c); break;
+        case 1: domino_sweep_kernel<1><<<grid, block, 0, stream>>>(c); break;
+        default: domino_sweep_kernel<2><<<grid, block, 0, stream>>>(c); break;
     }
     TSB_CUDA(cudaGetLastError());
     h->cur ^= 1;
+    return TSB_OK;
+}
+
+__global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
+__global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
+
+// A CUDA graph of kGraphSweeps sweeps (even, so the buffers end where they
+// started) followed by `step += kGraphSweeps`; long walks replay it, which
+// removes the per-launch host overhead (the kernels read the step base from
+// device memory).
+int ensure_graph(tsb_domino *h, int chain0, int n) {
+    const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
+                      h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1;
+    if (same) return TSB_OK;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    if (!h->cap_stream) TSB_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = TSB_OK;
+    for (int i = 0; i < kGraphSweeps && !rc; ++i)
+        rc = launch_sweep(h, chain0, n, (uint64_t)i, -1, h->cap_stream, h->step_dev);
+    advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+    e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        h->graph_exec = nullptr;
+        return cuda_fail(e, "graph instantiate");
+    }
+    h->g_chain0 = chain0;
+    h->g_n = n;
+    h->g_cur = h->cur;
+    h->g_tmode = h->tmode;
+    h->g_t0 = h->t0;
+    h->g_t1 = h->t1;
     return TSB_OK;
 }
 
@@ -380,6 +429,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
         return bail(e, "cudaMallocHost seeds");
     if ((e = cudaMalloc(&h->bad, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc flag");
+    if ((e = cudaMalloc(&h->step_dev, sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
     if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess)
         return bail(e, "cudaEventCreate");
     if ((e = cudaEventRecord(h->seed_ev, h->stream)) != cudaSuccess) return bail(e, "cudaEventRecord");
@@ -400,6 +450,27 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     e = cudaStreamSynchronize(h->stream);
     cudaFree(dfaces);
     if (e != cudaSuccess) return bail(e, "domain planes");
+    // non-empty sweep tiles (kTileRows rows x kTileWords output words)
+    std::vector<int2> rg(side);
+    if ((e = cudaMemcpy(rg.data(), h->range, sizeof(int2) * side, cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return bail(e, "ranges");
+    std::vector<int2> tiles;
+    const int nchunks = (h->W + 1 + kTileWords - 1) / kTileWords;
+    for (int y = 0; y * kTileRows < side; ++y) {
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int r = y * kTileRows; r < std::min(side, (y + 1) * kTileRows); ++r)
+            if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
+        for (int x = 0; x < nchunks; ++x) {
+            const int w0 = x * kTileWords - 1;
+            if (hi > w0 && lo < w0 + kTileWords) tiles.push_back(make_int2(x, y));
+        }
+    }
+    h->ntiles = (int)tiles.size();
+    if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
+        return bail(e, "cudaMalloc tiles");
+    if (!tiles.empty() &&
+        (e = cudaMemcpy(h->tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(e, "tiles");
     *out = h;
     return TSB_OK;
 }
@@ -413,10 +484,14 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->dom);
     cudaFree(h->fbits);
     cudaFree(h->range);
+    cudaFree(h->tiles);
     cudaFree(h->tgrid);
     cudaFree(h->seedinfo);
     cudaFree(h->bytes);
     cudaFree(h->bad);
+    cudaFree(h->step_dev);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->seed_pinned) cudaFreeHost(h->seed_pinned);
     if (h->seed_ev) cudaEventDestroy(h->seed_ev);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -510,8 +585,15 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
     if (!seeds) return fail(TSB_E_VALUE, "null seeds");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
-    for (uint64_t s = 0; s < n_steps; ++s)
-        if ((rc = launch_sweep(h, chain0, n, step0 + s, -1))) return rc;
+    uint64_t s = 0;
+    if (n_steps >= 2 * kGraphSweeps) {
+        if ((rc = ensure_graph(h, chain0, n))) return rc;
+        set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        TSB_CUDA(cudaGetLastError());
+        for (; s + kGraphSweeps <= n_steps; s += kGraphSweeps) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
+    }
+    for (; s < n_steps; ++s)
+        if ((rc = launch_sweep(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;
     return settle(h, chain0, n, n_steps);
 }
 
@@ -521,7 +603,7 @@ int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, ui
     if (color != 0 && color != 1) return fail(TSB_E_VALUE, "colour must be 0 (BLACK) or 1 (WHITE)");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
-    if ((rc = launch_sweep(h, chain0, n, step, color))) return rc;
+    if ((rc = launch_sweep(h, chain0, n, step, color, h->stream, nullptr))) return rc;
     return settle(h, chain0, n, 1);
 }
 

@@ -11,6 +11,8 @@ struct tsb_domino {
     uint4 *dom = nullptr;        // {crossable V, crossable H, existing V, existing H} per word
     uint32_t *fbits = nullptr;   // face (r, c) in the domain
     int2 *range = nullptr;
+    int2 *tiles = nullptr;  // non-empty sweep tiles {word chunk, row band}
+    int ntiles = 0;
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;
@@ -22,13 +24,22 @@ struct tsb_domino {
     int *bad = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // CUDA graph of kGraphSweeps sweeps, replayed by long walks
+    uint64_t *step_dev = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
+    uint64_t g_t0 = 0, g_t1 = 0;
 };
+
+constexpr int kGraphSweeps = 32;
 
 
 namespace tsb {
 int ensure_bytes(tsb_domino *h, size_t need);
 int check_range(tsb_domino *h, int chain0, int n);
 int push_seeds(tsb_domino *h, int n, const uint64_t *seeds);
-int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override);
+int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override, cudaStream_t stream,
+                 const uint64_t *step_dev);
 int settle(tsb_domino *h, int chain0, int n, uint64_t nsweeps);
 }  // namespace tsb

@@ -80,6 +80,21 @@ def test_walk_vs_oracle_aztec(order, steps, seed):
     assert np.array_equal(out, ref)
 
 
+def test_walk_vs_oracle_multi_chunk():
+    """Rows wider than one warp tile (62 words = 1984 columns): tile seams,
+    per-site thresholds (mode 2) and the graph + remainder launch path."""
+    d = ts.Domain.aztec(1100)
+    plan = ts.SweepPlan(d, ts.VolumeWeights(1.01, {(1100, 1100): 5.0, (1100, 1985): 0.2}))
+    t_max, _ = ts.lattice.aztec_extremal_states(1100)
+    out = ts.random_walk_batch(t_max[None], [77], 75, plan)
+    ref = oracle.domino_walk(t_max[None], [77], plan.p_up, 75, threads=8)
+    assert np.array_equal(out, ref)
+    # a mixed start (coins active across the seams)
+    out2 = ts.random_walk_batch(out, [78], 70, ts.SweepPlan(d))
+    ref2 = oracle.domino_walk(ref, [78], np.full_like(plan.p_up, 0.5), 70, threads=8)
+    assert np.array_equal(out2, ref2)
+
+
 def test_walk_vs_oracle_weighted_square():
     d = ts.Domain.square(70)
     w = ts.VolumeWeights(0.8, {(5, 5): 3.0, (69, 1): 0.1})
