@@ -39,7 +39,8 @@ enum {
     TSB_E_NODEVICE = 5,     /* RuntimeError: no sm_100 device                 */
     TSB_E_CONVERGENCE = 6,  /* ConvergenceCapExceeded (errors.py:64-65)       */
     TSB_E_DOMAIN = 7,       /* DomainError          (errors.py:8-9)           */
-    TSB_E_UNTILEABLE = 8    /* UntileableDomain     (errors.py:56-57)         */
+    TSB_E_UNTILEABLE = 8,   /* UntileableDomain     (errors.py:56-57)         */
+    TSB_E_INFEASIBLE = 9    /* InfeasibleBoundary   (errors.py:52-53)         */
 };
 
 /* ---------------------------------------------------------------- library */
@@ -120,6 +121,40 @@ int tsb_domino_replicate(tsb_domino *h, int src, int dst0, int step, int n);
 int tsb_domino_cftp(tsb_domino *h, const uint8_t *top0, const uint8_t *bot0, const uint64_t *masters,
                     int count, int max_doublings, uint8_t *out_states, int32_t *collapsed_round,
                     tsb_progress_fn progress, void *user);
+
+/* ------------------------------------------------------------- six-vertex */
+typedef struct tsb_sv tsb_sv;
+
+/* `nchains` six-vertex chains on the n x n vertex grid; state = face heights
+ * (n+1) x (n+1) int32 (FaceHeights, sixvertex.py:199-210), stored on the
+ * device as one bit per face (h mod 4). */
+int tsb_sv_create(int device, int n, int nchains, tsb_sv **out);
+int tsb_sv_destroy(tsb_sv *h);
+int tsb_sv_set_stream(tsb_sv *h, void *stream);
+/* Heat-bath p_high for the 32 local patterns: index (max ? 16 : 0) | NW<<3 |
+ * NE<<2 | SW<<1 | SE, where a diagonal bit is set when that diagonal face
+ * differs from the centre by 2 (sixvertex.py:354-442). */
+int tsb_sv_set_p_high(tsb_sv *h, const double *p_high);
+/* Height batches (n, n+1, n+1) int32; upload rejects grids whose adjacent
+ * faces do not differ by exactly 1 (TSB_E_INCONSISTENT). */
+int tsb_sv_upload(tsb_sv *h, int chain0, int n, const int32_t *heights);
+int tsb_sv_download(tsb_sv *h, int chain0, int n, int32_t *heights);
+/* sv_random_walk_batch (sixvertex.py:445-467): class from the global coin. */
+int tsb_sv_walk(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uint64_t step0, uint64_t n_steps);
+/* sv_sweep (sixvertex.py:470-486): one sweep of an explicit face class 0..3. */
+int tsb_sv_sweep(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int face_class);
+int tsb_sv_sync(tsb_sv *h);
+/* sv_extremal (sixvertex.py:534-562) from the ring heights of
+ * _ring_heights (ring: (n+1)^2 int32, interior ignored) into chains
+ * chain_max / chain_min; heights to hmax / hmin (nullable).
+ * TSB_E_INFEASIBLE when the ring heights are incompatible. */
+int tsb_sv_extremal(tsb_sv *h, const int32_t *ring, int chain_max, int chain_min, int32_t *hmax, int32_t *hmin);
+int tsb_sv_coalesced(tsb_sv *h, int chain0, int npairs, uint8_t *flags);
+int tsb_sv_replicate(tsb_sv *h, int src, int dst0, int step, int n);
+/* sv_cftp (sixvertex.py:565-622): as tsb_domino_cftp with height grids. */
+int tsb_sv_cftp(tsb_sv *h, const int32_t *top0, const int32_t *bot0, const uint64_t *masters, int count,
+                int max_doublings, int32_t *out_heights, int32_t *collapsed_round, tsb_progress_fn progress,
+                void *user);
 
 /* One-shot form of the fused hook: evolves a host (nchains, side, side)
  * uint8 batch in place (upload + walk + download). */

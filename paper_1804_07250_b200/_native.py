@@ -33,7 +33,8 @@ _lock = threading.Lock()
 _device = int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("TSB_DEVICE") is None else int(
     os.environ["TSB_DEVICE"])
 
-OK, E_VALUE, E_INCONSISTENT, E_CAPACITY, E_CUDA, E_NODEVICE, E_CONVERGENCE, E_DOMAIN, E_UNTILEABLE = range(9)
+(OK, E_VALUE, E_INCONSISTENT, E_CAPACITY, E_CUDA, E_NODEVICE, E_CONVERGENCE, E_DOMAIN, E_UNTILEABLE,
+ E_INFEASIBLE) = range(10)
 _EXC = {
     E_VALUE: ValueError,
     E_INCONSISTENT: errors.InconsistencyError,
@@ -43,6 +44,7 @@ _EXC = {
     E_CONVERGENCE: errors.ConvergenceCapExceeded,
     E_DOMAIN: errors.DomainError,
     E_UNTILEABLE: errors.UntileableDomain,
+    E_INFEASIBLE: errors.InfeasibleBoundary,
 }
 
 
@@ -92,6 +94,19 @@ _SIGS = {
     "tsb_domino_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_replicate": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_cftp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "tsb_sv_create": (_i, [_i, _i, _i, _vp]),
+    "tsb_sv_destroy": (_i, [_vp]),
+    "tsb_sv_set_stream": (_i, [_vp, _vp]),
+    "tsb_sv_set_p_high": (_i, [_vp, _vp]),
+    "tsb_sv_upload": (_i, [_vp, _i, _i, _vp]),
+    "tsb_sv_download": (_i, [_vp, _i, _i, _vp]),
+    "tsb_sv_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),
+    "tsb_sv_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
+    "tsb_sv_sync": (_i, [_vp]),
+    "tsb_sv_extremal": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
+    "tsb_sv_coalesced": (_i, [_vp, _i, _i, _vp]),
+    "tsb_sv_replicate": (_i, [_vp, _i, _i, _i, _i]),
+    "tsb_sv_cftp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
 }
 
 

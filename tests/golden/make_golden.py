@@ -166,6 +166,19 @@ def make_sixvertex():
         hi, lo = ts.sv_extremal(n, ts.dwbc(n))
         arrays[f"e{n}_hi"] = hi.heights
         arrays[f"e{n}_lo"] = lo.heights
+    # p_high of the 32 flippable 3x3 patterns via the reference's own
+    # sv_heat_bath_p_up (sixvertex.py:318-337), for the LUT check
+    from tilesampler.sixvertex import sv_heat_bath_p_up
+    for j, weights in enumerate(gc.SV_LUT_WEIGHTS):
+        lut = []
+        for idx in range(32):
+            s_ = -1 if idx >= 16 else 1
+            h = np.zeros((3, 3), dtype=np.int32)
+            h[0, 1] = h[2, 1] = h[1, 0] = h[1, 2] = s_
+            for bit, (r, c) in zip((8, 4, 2, 1), ((0, 0), (0, 2), (2, 0), (2, 2))):
+                h[r, c] = 2 * s_ if idx & bit else 0
+            lut.append(sv_heat_bath_p_up(ts.FaceHeights(2, h), (1, 1), ts.SVWeights(*weights)))
+        arrays[f"lut{j}"] = np.array(lut)
     # CFTP on DWBC 3 / 4
     for j, (n, weights, master, count) in enumerate(gc.SV_CFTP_CASES):
         trace = ts.CftpTrace()

@@ -174,6 +174,7 @@ SV_CASES = [
     (24, (2.0, 0.5, 1.0), 4242, 200, "min"),
 ]
 SV_EXTREMAL_N = [1, 2, 3, 5, 8, 13]
+SV_LUT_WEIGHTS = [(1.0, 1.0, 1.0), (1.0, 1.0, math.sqrt(8.0)), (0.7, 1.3, 1.9), (2.0, 0.5, 1.0), (1.0, 1.0, 0.3)]
 SV_CFTP_CASES = [(3, (1.0, 1.0, 1.0), 11, 5), (4, (1.0, 1.0, 1.5), 2024, 3)]
 
 # lozenges: ((a, b, c), weights, seed, n_steps, start)

@@ -144,3 +144,28 @@ def test_cftp_schedule_prepends():
     with pytest.raises(ts.ConvergenceCapExceeded):
         sched.grow()
         sched.grow()
+
+
+def test_sixvertex_p_high_lut_matches_reference():
+    from paper_1804_07250_b200.sixvertex import p_high_lut
+
+    g = load("sixvertex.npz")
+    for j, w in enumerate(gc.SV_LUT_WEIGHTS):
+        assert np.array_equal(p_high_lut(ts.SVWeights(*w)), g[f"lut{j}"]), w
+
+
+def test_sixvertex_codecs_and_ring():
+    from paper_1804_07250_b200.sixvertex import _ring_heights
+
+    g = load("sixvertex.npz")
+    for n in gc.SV_EXTREMAL_N:
+        for key in ("hi", "lo"):
+            fh = ts.FaceHeights(n, g[f"e{n}_{key}"])
+            cfg = ts.config_from_heights(fh)
+            assert ts.heights_from_config(cfg) == fh
+        ring = _ring_heights(ts.dwbc(n))
+        hi = g[f"e{n}_hi"]
+        assert np.array_equal(ring[0], hi[0]) and np.array_equal(ring[:, 0], hi[:, 0])
+    bad = ts.Boundary(2, top=[1, 1], bottom=[0, 0], left=[0, 0], right=[0, 0])
+    with pytest.raises(ts.InfeasibleBoundary):
+        _ring_heights(bad)

@@ -1,0 +1,100 @@
+"""Six-vertex parity on the device vs the reference's golden outputs and the
+C oracle (bit-exact integer heights)."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import oracle
+import paper_1804_07250_b200 as ts
+from paper_1804_07250_b200.sixvertex import SixVertexHandle, p_high_lut, sv_random_walk_batch
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(G, name))
+
+
+def closed_form(n):
+    R, C = np.meshgrid(np.arange(n + 1), np.arange(n + 1), indexing="ij")
+    return -np.abs(R - C), np.maximum(-(R + C), R + C - 2 * n)
+
+
+def test_golden_walks():
+    g = load("sixvertex.npz")
+    for i, (n, w, seed, steps, _) in enumerate(gc.SV_CASES):
+        out = sv_random_walk_batch(g[f"v{i}_start"][None], [seed], steps, ts.SVWeights(*w))
+        assert np.array_equal(out[0], g[f"v{i}_out"]), f"sv case {i}"
+
+
+def test_golden_extremal():
+    g = load("sixvertex.npz")
+    for n in gc.SV_EXTREMAL_N:
+        hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+        assert np.array_equal(hi.heights, g[f"e{n}_hi"]) and np.array_equal(lo.heights, g[f"e{n}_lo"])
+
+
+@pytest.mark.parametrize("n", [64, 300, 2048])
+def test_extremal_closed_form(n):
+    hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+    chi, clo = closed_form(n)
+    assert np.array_equal(hi.heights, chi) and np.array_equal(lo.heights, clo)
+
+
+@pytest.mark.parametrize("n,w,steps", [(200, (1.0, 1.0, 1.0), 400), (257, (1.0, 1.0, math.sqrt(8.0)), 333),
+                                       (97, (0.6, 1.4, 2.0), 500)])
+def test_walk_vs_oracle(n, w, steps):
+    hi, lo = closed_form(n)
+    start = np.stack([lo, hi, lo]).astype(np.int32)
+    seeds = np.array([1, 2, 2**63 + 3], dtype=np.uint64)
+    weights = ts.SVWeights(*w)
+    out = sv_random_walk_batch(start, seeds, steps, weights)
+    ref = oracle.sv_walk(start, seeds, weights.table(), steps)
+    assert np.array_equal(out, ref)
+    # continuation: split walks equal one walk
+    h = SixVertexHandle(n, 3)
+    h.set_weights(weights)
+    h.upload(start)
+    h.walk(seeds, steps // 2)
+    h.walk(seeds, steps - steps // 2, step0=steps // 2)
+    assert np.array_equal(h.download(), ref)
+
+
+def test_sweep_and_errors():
+    n = 6
+    hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+    cfg = ts.config_from_heights(lo)
+    fam = ts.seed_family(5, (n + 1, n + 1))
+    for k in range(4):
+        out = ts.sv_sweep(cfg, fam, 3, k, ts.SVWeights())
+        ts.heights_from_config(out)  # valid configuration
+    bad = lo.heights.copy()
+    bad[3, 3] += 5
+    with pytest.raises(ts.InconsistencyError):
+        sv_random_walk_batch(bad[None], [1], 1, ts.SVWeights())
+    with pytest.raises(ts.NonMonotoneWeights):
+        ts.sv_cftp(3, ts.dwbc(3), ts.SVWeights(2.0, 1.0, 1.0), 1)
+
+
+def test_cftp_golden():
+    g = load("sixvertex.npz")
+    for j, (n, w, master, count) in enumerate(gc.SV_CFTP_CASES):
+        trace = ts.CftpTrace()
+        res = ts.sv_cftp(n, ts.dwbc(n), ts.SVWeights(*w), master, count=count, trace=trace)
+        res = res if isinstance(res, list) else [res]
+        hs = np.stack([ts.heights_from_config(c).heights for c in res])
+        assert np.array_equal(hs, g[f"k{j}_h"]), f"cftp {j}"
+        assert trace.collapsed_at == int(g[f"k{j}_collapsed"])
+
+
+def test_sweep_stays_monotone_coupled():
+    """Grand coupling: the walk from h_max stays above the walk from h_min."""
+    n = 40
+    hi, lo = closed_form(n)
+    out = sv_random_walk_batch(np.stack([hi, lo]).astype(np.int32), [9, 9], 300, ts.SVWeights(1, 1, 1.5))
+    assert (out[0] >= out[1]).all()
