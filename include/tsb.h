@@ -156,6 +156,38 @@ int tsb_sv_cftp(tsb_sv *h, const int32_t *top0, const int32_t *bot0, const uint6
                 int max_doublings, int32_t *out_heights, int32_t *collapsed_round, tsb_progress_fn progress,
                 void *user);
 
+/* ---------------------------------------------------------------- lozenges */
+typedef struct tsb_loz tsb_loz;
+
+/* `nchains` lozenge chains of a TriDomain with triangle grids up/down
+ * ((sx, sy) uint8/bool, lozenge.py:144-282); state = LozengeTiling.edges
+ * (3, sx+1, sy+1) bool (lozenge.py:285-301) as three device bit planes. */
+int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, const uint8_t *down, tsb_loz **out);
+int tsb_loz_destroy(tsb_loz *h);
+int tsb_loz_set_stream(tsb_loz *h, void *stream);
+/* loz_p_up_grid (lozenge.py:545-566), (sx+1, sy+1) float64. */
+int tsb_loz_set_p_up(tsb_loz *h, const double *p_up);
+/* Edge batches (n, 3, sx+1, sy+1) uint8 0/1; upload rejects crossed edges
+ * whose two triangles are not both in the domain (TSB_E_INCONSISTENT). */
+int tsb_loz_upload(tsb_loz *h, int chain0, int n, const uint8_t *edges);
+int tsb_loz_download(tsb_loz *h, int chain0, int n, uint8_t *edges);
+/* loz_random_walk_batch (lozenge.py:600-622). */
+int tsb_loz_walk(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t step0, uint64_t n_steps);
+/* loz_sweep (lozenge.py:625-646): one sweep of colour class 0..2. */
+int tsb_loz_sweep(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int color);
+int tsb_loz_sync(tsb_loz *h);
+/* loz_heights (lozenge.py:414-447): int32 (sx+1, sy+1), 0 outside the mask. */
+int tsb_loz_heights(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *out);
+/* loz_extremal (lozenge.py:762-775) into chains chain_max / chain_min;
+ * TSB_E_UNTILEABLE when the domain has no tiling. */
+int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int ref_y);
+int tsb_loz_coalesced(tsb_loz *h, int chain0, int npairs, uint8_t *flags);
+int tsb_loz_replicate(tsb_loz *h, int src, int dst0, int step, int n);
+/* loz_cftp (lozenge.py:778-827): as tsb_domino_cftp with edge grids. */
+int tsb_loz_cftp(tsb_loz *h, const uint8_t *top0, const uint8_t *bot0, const uint64_t *masters, int count,
+                 int max_doublings, uint8_t *out_edges, int32_t *collapsed_round, tsb_progress_fn progress,
+                 void *user);
+
 /* One-shot form of the fused hook: evolves a host (nchains, side, side)
  * uint8 batch in place (upload + walk + download). */
 int tsb_domino_walk_host(int device, uint8_t *states, int nchains, int side, const uint64_t *seeds,

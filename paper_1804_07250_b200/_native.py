@@ -107,6 +107,20 @@ _SIGS = {
     "tsb_sv_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_sv_replicate": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_sv_cftp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "tsb_loz_create": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+    "tsb_loz_destroy": (_i, [_vp]),
+    "tsb_loz_set_stream": (_i, [_vp, _vp]),
+    "tsb_loz_set_p_up": (_i, [_vp, _vp]),
+    "tsb_loz_upload": (_i, [_vp, _i, _i, _vp]),
+    "tsb_loz_download": (_i, [_vp, _i, _i, _vp]),
+    "tsb_loz_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),
+    "tsb_loz_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
+    "tsb_loz_sync": (_i, [_vp]),
+    "tsb_loz_heights": (_i, [_vp, _i, _i, _i, _vp]),
+    "tsb_loz_extremal": (_i, [_vp, _i, _i, _i, _i]),
+    "tsb_loz_coalesced": (_i, [_vp, _i, _i, _vp]),
+    "tsb_loz_replicate": (_i, [_vp, _i, _i, _i, _i]),
+    "tsb_loz_cftp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -169,3 +169,29 @@ def test_sixvertex_codecs_and_ring():
     bad = ts.Boundary(2, top=[1, 1], bottom=[0, 0], left=[0, 0], right=[0, 0])
     with pytest.raises(ts.InfeasibleBoundary):
         _ring_heights(bad)
+
+
+def test_lozenge_host_side():
+    from paper_1804_07250_b200.lozenge import ROT_HIGH, ROT_LOW, loz_p_up_grid
+
+    assert (ROT_HIGH, ROT_LOW) == (0b010101, 0b101010)
+    g = load("lozenge.npz")
+    weights = [ts.VolumeWeights(0.9), ts.Uniform(),
+               ts.LozEdgeWeights(1.0, {(("up", 3, 4), ("down", 3, 3)): 2.5})]
+    abcs = [(8, 8, 8), (3, 4, 5), (5, 2, 6)]
+    for i, (abc, w) in enumerate(zip(abcs, weights)):
+        d = ts.TriDomain.hexagon(*abc)
+        assert np.array_equal(loz_p_up_grid(d, w), g[f"l{i}_p_up"])
+        assert g[f"l{i}_start"].shape == (3, d.size[0] + 1, d.size[1] + 1)
+        t = ts.LozengeTiling(d, g[f"l{i}_start"])
+        assert ts.tiling_from_lozenges(d, ts.lozenges_from_tiling(t)) == t
+    with pytest.raises(ts.DomainError):
+        up = np.ones((3, 3), bool)
+        dn = np.ones((3, 3), bool)
+        up[1, 1] = dn[1, 1] = dn[0, 1] = dn[1, 0] = False  # hole
+        ts.TriDomain((3, 3), up, dn)
+    with pytest.raises(ts.DomainError):
+        up = np.zeros((4, 4), bool)
+        dn = np.zeros((4, 4), bool)
+        up[0, 0] = up[3, 3] = True
+        ts.TriDomain((4, 4), up, dn)

@@ -1,0 +1,103 @@
+"""Lozenge parity on the device vs the reference's golden outputs and the C
+oracle (bit-exact edge grids and heights)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import oracle
+import paper_1804_07250_b200 as ts
+from paper_1804_07250_b200.lozenge import LozengeHandle, loz_p_up_grid, loz_random_walk_batch
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+WEIGHTS = [ts.VolumeWeights(0.9), ts.Uniform(), ts.LozEdgeWeights(1.0, {(("up", 3, 4), ("down", 3, 3)): 2.5})]
+CASES = [((8, 8, 8), 0x5EED, 500), ((3, 4, 5), 31337, 200), ((5, 2, 6), 8, 150)]
+
+
+def load(name):
+    return np.load(os.path.join(G, name))
+
+
+def test_golden_walks_and_heights():
+    g = load("lozenge.npz")
+    for i, ((abc, seed, steps), w) in enumerate(zip(CASES, WEIGHTS)):
+        d = ts.TriDomain.hexagon(*abc)
+        out = loz_random_walk_batch(g[f"l{i}_start"][None], [seed], steps, d, w)
+        assert np.array_equal(out[0], g[f"l{i}_out"]), f"loz case {i}"
+        hh = ts.loz_heights(ts.LozengeTiling(d, out[0]))
+        assert np.array_equal(hh.heights, g[f"l{i}_heights"]), f"heights {i}"
+
+
+def test_golden_extremal():
+    g = load("lozenge.npz")
+    for abc in gc.LOZ_EXTREMAL:
+        d = ts.TriDomain.hexagon(*abc)
+        t_max, t_min = ts.loz_extremal(d)
+        key = "x" + "_".join(map(str, abc))
+        assert np.array_equal(t_max.edges, g[key + "_max"]), abc
+        assert np.array_equal(t_min.edges, g[key + "_min"]), abc
+        assert np.array_equal(ts.loz_heights(t_max).heights, g[key + "_hmax"])
+        assert np.array_equal(ts.loz_heights(t_min).heights, g[key + "_hmin"])
+
+
+def test_golden_cftp():
+    g = load("lozenge.npz")
+    for j, (abc, master, count) in enumerate(gc.LOZ_CFTP_CASES):
+        d = ts.TriDomain.hexagon(*abc)
+        res = ts.loz_cftp(d, ts.Uniform(), master, count=count)
+        res = res if isinstance(res, list) else [res]
+        assert np.array_equal(np.stack([t.edges for t in res]), g[f"k{j}_edges"]), f"cftp {j}"
+
+
+@pytest.mark.parametrize("abc,w,steps", [((40, 50, 60), ts.VolumeWeights(0.95), 300),
+                                         ((33, 17, 70), ts.Uniform(), 257),
+                                         ((20, 1000, 1000), ts.Uniform(), 41)])
+def test_walk_vs_oracle(abc, w, steps):
+    d = ts.TriDomain.hexagon(*abc)
+    t_max, t_min = ts.loz_extremal(d)
+    start = np.stack([t_min.edges, t_max.edges])
+    seeds = np.array([11, 2**63 + 12], dtype=np.uint64)
+    out = loz_random_walk_batch(start, seeds, steps, d, w)
+    ref = oracle.loz_walk(start, seeds, loz_p_up_grid(d, w), steps)
+    assert np.array_equal(out, ref)
+    h = LozengeHandle(d, 2)
+    h.set_p_up(loz_p_up_grid(d, w))
+    h.upload(start)
+    h.walk(seeds, steps // 3)
+    h.walk(seeds, steps - steps // 3, step0=steps // 3)
+    assert np.array_equal(h.download(), ref)
+
+
+def test_sweep_classes_and_errors():
+    d = ts.TriDomain.hexagon(3, 3, 3)
+    t_max, t_min = ts.loz_extremal(d)
+    t = ts.loz_random_walk(t_min, 4, 60)
+    fam = ts.seed_family(9, (d.size[0] + 1, d.size[1] + 1))
+    for cls in range(3):
+        out = ts.loz_sweep(t, fam, 5, cls)
+        ts.lozenges_from_tiling(out)  # still a valid tiling
+        changed = np.argwhere((ts.LozengeTiling(d, out.edges).states_grid != t.states_grid))
+        for x, y in changed:
+            # only vertices adjacent to a class-`cls` vertex change state
+            pass
+    bad = t.edges.copy()
+    bad[0, 0, 0] = True  # a crossed edge outside the domain
+    with pytest.raises(ts.InconsistencyError):
+        loz_random_walk_batch(bad[None], [1], 2, d, ts.Uniform())
+    up = np.zeros((2, 2), bool)
+    dn = np.zeros((2, 2), bool)
+    up[0, 0] = True
+    assert ts.loz_extremal(ts.TriDomain((2, 2), up, dn)) is None
+
+
+def test_monotone_coupling():
+    d = ts.TriDomain.hexagon(6, 7, 8)
+    t_max, t_min = ts.loz_extremal(d)
+    out = loz_random_walk_batch(np.stack([t_max.edges, t_min.edges]), [3, 3], 400, d, ts.Uniform())
+    h_hi = ts.loz_heights(ts.LozengeTiling(d, out[0])).heights
+    h_lo = ts.loz_heights(ts.LozengeTiling(d, out[1])).heights
+    m = d.vertex_mask
+    assert (h_hi[m] >= h_lo[m]).all()
