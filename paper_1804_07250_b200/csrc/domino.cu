@@ -32,149 +32,173 @@ namespace tsb {
 
 constexpr int kTileRows = 15;   // output rows per block tile (+1 halo fire row)
 constexpr int kTileWords = 62;  // output words per tile: 64 loaded (2 per lane), 1 halo word each side
+constexpr int kPad = 2;         // zero words left of every state row (lane 0's halo of the first tile)
 
 struct SweepCtx {
-    const uint2 *src;
+    const uint2 *src;          // chain 0, row 0, word 0 (after the kPad left pad)
     uint2 *dst;
-    const int2 *range;         // [side] word range [lo, hi) that can hold set bits
     const uint64_t *seedinfo;  // [n][2] = {family base, global key}
     const uint64_t *tgrid;     // per-site thresholds (mode 2), (side x side)
-    const uint64_t *step_dev;  // graph replays: step = *step_dev + step (nullable)
-    const int2 *tiles;         // non-empty tiles {word chunk, row band}
+    const uint64_t *step_dev;  // graph replays: step = *step_dev + step
     int ntiles;
+    const uint8_t *colors;     // graph replays: [n][kGraphSweeps] colours (null: direct launch)
+    const int2 *tiles;         // non-empty tiles {word chunk, row band}
     uint64_t t0, t1;           // thresholds for even / odd parity (modes 0, 1)
     size_t chain_stride;       // uint2 per chain (incl. guard rows)
-    int side, W, pitch;
+    int side, pitch;
     uint64_t step;
-    int color_override;  // -1: colour from the global coin
+    int color_override;  // -1: colour from the global coin (direct launches)
 };
 
-// Cold path: draw the heat-bath coin of every rotateable active vertex of a
-// word (bits of `rot`) and return the ones that move: 3 -> 12 when
-// u < p_up, 12 -> 3 otherwise (_kernels.py:49-55, sweeps.py:102-110).  Only
-// rotateable sites pay for the two splitmix64 rounds; counter-based draws
-// make the skipping exact.
+// Heat-bath coins of a warp's rotateable active vertices, load-balanced.
+// Each lane owns two words (bits `ra`, `rb` rotateable; `ia`, `ib`: state 3).
+// The warp's sites are queued in shared memory and dealt round-robin to the
+// lanes, two independent splitmix64 chains per lane per iteration, so a word
+// full of rotateable sites no longer serialises its lane (dense mixed states).
+// A site moves 3 -> 12 when u < p_up and 12 -> 3 otherwise
+// (_kernels.py:49-55, sweeps.py:102-110); only rotateable sites are drawn and
+// counter-based draws make the skipping exact.
 template <int TM>
-__device__ __noinline__ uint32_t rng_fire(uint32_t rot, uint32_t is3, uint64_t row_idx, int w,
-                                          uint64_t base, uint64_t salt, uint64_t t,
-                                          const uint64_t *__restrict__ tgrid) {
-    uint32_t fire = 0;
-    do {
-        const int b = __ffs(rot) - 1;
-        rot &= rot - 1;
-        const uint64_t idx = row_idx + (uint64_t)(w * 32 + b);  // r * side + c
-        const uint64_t x = mix64(mix64(base + (idx + 1ull) * kGold) + salt);
-        const uint64_t tt = TM == 2 ? __ldg(tgrid + idx) : t;
-        const bool up = (x >> 11) < tt;
-        if (up == (bool)((is3 >> b) & 1u)) fire |= 1u << b;
-    } while (rot);
-    return fire;
+__device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, uint32_t ib, uint16_t *queue,
+                                        uint32_t *fres, const uint64_t *__restrict__ seedinfo,
+                                        const uint64_t *__restrict__ tgrid, uint64_t t, int side, int z, int r,
+                                        int wa, uint64_t step) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = __popc(ra) + __popc(rb);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - cnt;
+    // job = is3 << 11 | lane << 6 | word << 5 | bit
+    for (uint32_t m = ra; m; m &= m - 1) {
+        const int b = __ffs(m) - 1;
+        queue[pos++] = (uint16_t)((((ia >> b) & 1u) << 11) | (lane << 6) | b);
+    }
+    for (uint32_t m = rb; m; m &= m - 1) {
+        const int b = __ffs(m) - 1;
+        queue[pos++] = (uint16_t)((((ib >> b) & 1u) << 11) | (lane << 6) | 32 | b);
+    }
+    fres[2 * lane] = 0u;
+    fres[2 * lane + 1] = 0u;
+    __syncwarp();
+    const uint64_t base = seedinfo[2 * z];
+    const uint64_t salt = (step + 1ull) * kGold;
+    // site index r * side + column; column = 32 * (wa of lane 0) + 64 * lane + 32 * word + bit
+    const uint64_t row_idx = (uint64_t)r * (uint64_t)side + (uint64_t)(int64_t)((wa - 2 * lane) * 32);
+    for (int j = lane; j < total; j += 64) {
+        const bool two = j + 32 < total;
+        const uint32_t q0 = queue[j], q1 = two ? queue[j + 32] : q0;
+        const uint64_t i0 = row_idx + (uint64_t)(q0 & 63u) + (uint64_t)(((q0 >> 6) & 31u) * 64u);
+        const uint64_t i1 = row_idx + (uint64_t)(q1 & 63u) + (uint64_t)(((q1 >> 6) & 31u) * 64u);
+        // two independent chains for ILP
+        const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
+        const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
+        const uint64_t t0 = TM == 2 ? __ldg(tgrid + i0) : t;
+        const uint64_t t1 = TM == 2 ? __ldg(tgrid + i1) : t;
+        if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+        if (two && ((x1 >> 11) < t1) == (bool)(q1 >> 11)) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
+    }
+    __syncwarp();
+    return make_uint2(fres[2 * lane], fres[2 * lane + 1]);
 }
 
-// Fire mask of one 32-column word of active vertices.
+// One sweep, one block per non-empty tile of kTileRows x 62 words (512
+// threads).  Warp k owns row r = r0+k; each lane owns two adjacent words
+// (16-byte loads; lanes 0 and 31 hold one halo word each, so horizontal
+// neighbours are shuffles).  Rows carry kPad zero words on the left and zero
+// padding on the right, and every word outside the domain is zero, so loads
+// need no predication.
+//   phase 0: V of every row -> shared (the row above for the fire test)
+//   phase 1: fire row F(r) of every row (warp 15 = halo row r0+15) -> shared
+//   phase 2: warps 0..14 toggle the four incident edges of every firing vertex:
+//            V[r] ^= F(r) ^ F(r+1),   H[r] ^= F(r) ^ F(r) >> 1 (carry from the next word).
 template <int TM>
-__device__ __forceinline__ uint32_t fire_mask(uint32_t vu, uint32_t vd, uint32_t h, uint32_t hleft,
-                                              uint32_t act, uint64_t row_idx, int w, uint64_t base,
-                                              uint64_t salt, uint64_t t, const uint64_t *tgrid) {
-    const uint32_t l = (h << 1) | (hleft >> 31);
-    const uint32_t is3 = vu & vd & ~(l | h) & act;
-    const uint32_t is12 = ~(vu | vd) & l & h & act;
-    const uint32_t rot = is3 | is12;
-    return rot ? rng_fire<TM>(rot, is3, row_idx, w, base, salt, t, tgrid) : 0u;
-}
-
-template <bool COHERENT>
-__device__ __forceinline__ uint4 ld16(const uint2 *p) {
-    return COHERENT ? __ldcg(reinterpret_cast<const uint4 *>(p)) : __ldg(reinterpret_cast<const uint4 *>(p));
-}
-template <bool COHERENT>
-__device__ __forceinline__ uint2 ld8(const uint2 *p) {
-    return COHERENT ? __ldcg(p) : __ldg(p);
-}
-
-// One tile of one sweep (kTileRows x 62 words, 512 threads).  Warp k owns
-// row r0+k (lane = two adjacent words, 16-byte loads; lanes 0 and 31 hold one
-// halo word each, so horizontal neighbours are shuffles).  Phase 1: every
-// warp computes the fire row F(r) of its row (warp 15 is the halo row r0+15)
-// into shared memory.  Phase 2: warps 0..14 toggle the four incident edges of
-// every firing vertex:
-//   V[r] ^= F(r) ^ F(r+1),   H[r] ^= F(r) ^ F(r) >> 1 (carry from the next word).
-// COHERENT loads (L2 only) are used by the persistent kernel, whose inputs are
-// written by other blocks during the same launch.
-template <int TM, bool COHERENT>
-__device__ __forceinline__ void sweep_tile(const SweepCtx &c, int2 tile, const uint2 *src, uint2 *dst,
-                                           uint64_t base, uint64_t salt, int color, uint2 (*fs)[32]) {
+__global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
+    domino_sweep_kernel(SweepCtx c) {
+    __shared__ uint2 vs[kTileRows + 1][32];
+    __shared__ uint2 fs[kTileRows + 1][32];
+    __shared__ uint16_t queue[kTileRows + 1][1024];
+    __shared__ uint32_t fres[kTileRows + 1][64];
     const int lane = threadIdx.x & 31;
     const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
     const int r = tile.y * kTileRows + k;
-    const int wout0 = tile.x * kTileWords - 1;  // first output word of the tile
-    const int wa = wout0 - 1 + 2 * lane, wb = wa + 1;
-    const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
-
-    // rows r-1 (V) and r (V, H); zero outside each row's word range
-    const bool live = r < c.side;
-    const int2 g = live ? __ldg(c.range + r) : make_int2(0, 0);
-    const int2 gm = (live && r > 0) ? __ldg(c.range + r - 1) : make_int2(0, 0);
-    const bool ina = wa >= g.x && wa < g.y, inb = wb >= g.x && wb < g.y;
-    const bool inma = wa >= gm.x && wa < gm.y, inmb = wb >= gm.x && wb < gm.y;
-    const uint2 *row = src + (ptrdiff_t)r * c.pitch;
+    const int wa = tile.x * kTileWords - 2 + 2 * lane;  // words wa, wa+1; outputs wa+1 .. wa+62 of lane 0..31
+    const int z = blockIdx.z;
+    const bool live = r < c.side;  // rows >= side are the zero guard row or beyond: never loaded / stored
+    const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    // Programmatic dependent launch: let the next sweep's grid start its
+    // prologue now, and wait for the previous sweep's stores before loading.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
-    if (ina && inb) cur = ld16<COHERENT>(row + wa);
-    else {
-        if (ina) { const uint2 x = ld8<COHERENT>(row + wa); cur.x = x.x; cur.y = x.y; }
-        if (inb) { const uint2 x = ld8<COHERENT>(row + wb); cur.z = x.x; cur.w = x.y; }
-    }
+    if (live) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
     uint32_t vua = 0, vub = 0;
-    if (inma && inmb) { const uint4 q = ld16<COHERENT>(row - c.pitch + wa); vua = q.x; vub = q.z; }
-    else {
-        if (inma) vua = ld8<COHERENT>(row - c.pitch + wa).x;
-        if (inmb) vub = ld8<COHERENT>(row - c.pitch + wb).x;
+    if (k == 0) {  // the tile's first row reads the row above from global (guard row at r = -1)
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row - c.pitch + wa));
+        vua = q.x;
+        vub = q.z;
+    }
+    // colour: per-replay table (graph mode) or the global coin; BLACK iff
+    // u < 1/2 <=> bit 63 of the draw is 0 (_kernels.py:44-45, sweeps.py:266-269)
+    int color;
+    uint64_t step;
+    if (c.colors) {
+        step = *c.step_dev + c.step;
+        color = c.colors[z * kGraphSweeps + (int)c.step];
+    } else {
+        step = c.step;
+        color = c.color_override >= 0 ? c.color_override
+                                      : (int)(mix64(c.seedinfo[2 * z + 1] + (step + 1ull) * kGold) >> 63);
+    }
+    vs[k][lane] = make_uint2(cur.x, cur.z);
+    __syncthreads();
+    if (k > 0) {
+        const uint2 u = vs[k - 1][lane];
+        vua = u.x;
+        vub = u.y;
     }
     // lane 0's first word is a pure halo (its fire row feeds no output); lane
     // 31's second word only feeds bit 0 into the H carry of its first word.
     const uint32_t act = ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u;
     const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
-    const uint64_t ridx = (uint64_t)r * (uint64_t)c.side;
-    const uint32_t fa = fire_mask<TM>(vua, cur.x, cur.y, hl, lane == 0 ? 0u : act, ridx, wa, base, salt, t, c.tgrid);
-    const uint32_t fb = fire_mask<TM>(vub, cur.z, cur.w, cur.y, lane == 31 ? act & 1u : act, ridx, wb, base, salt, t,
-                                      c.tgrid);
-    fs[k][lane] = make_uint2(fa, fb);
-    __syncthreads();
-    if (k < kTileRows && live) {  // warp-uniform
-        const uint2 fn = fs[k + 1][lane];  // F(r+1)
-        const uint32_t frb = __shfl_down_sync(0xffffffffu, fa, 1);
-        const uint32_t nva = cur.x ^ fa ^ fn.x;
-        const uint32_t nvb = cur.z ^ fb ^ fn.y;
-        const uint32_t nha = cur.y ^ fa ^ (fa >> 1) ^ (fb << 31);
-        const uint32_t nhb = cur.w ^ fb ^ (fb >> 1) ^ (frb << 31);
-        uint2 *out = dst + (ptrdiff_t)r * c.pitch;
-        const bool sa = lane > 0 && ina, sb = lane < 31 && inb;
-        if (sa && sb) *reinterpret_cast<uint4 *>(out + wa) = make_uint4(nva, nha, nvb, nhb);
-        else {
-            if (sa) out[wa] = make_uint2(nva, nha);
-            if (sb) out[wb] = make_uint2(nvb, nhb);
-        }
+    const uint32_t la = (cur.y << 1) | (hl >> 31);
+    const uint32_t ia = vua & cur.x & ~(la | cur.y);
+    const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & (lane == 0 ? 0u : act);
+    const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
+    const uint32_t ib = vub & cur.z & ~(lb | cur.w);
+    const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & (lane == 31 ? act & 1u : act);
+    uint2 f = make_uint2(0u, 0u);
+    if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
+        const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
+        f = warp_fire<TM>(ra, rb, ia, ib, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step);
     }
+    const uint32_t fa = f.x, fb = f.y;
+    fs[k][lane] = f;
+    __syncthreads();
+    if (k == kTileRows || !live) return;  // warp-uniform
+    const uint2 fn = fs[k + 1][lane];     // F(r+1)
+    const uint32_t frb = __shfl_down_sync(0xffffffffu, fa, 1);
+    const uint32_t nva = cur.x ^ fa ^ fn.x;
+    const uint32_t nvb = cur.z ^ fb ^ fn.y;
+    const uint32_t nha = cur.y ^ fa ^ (fa >> 1) ^ (fb << 31);
+    const uint32_t nhb = cur.w ^ fb ^ (fb >> 1) ^ (frb << 31);
+    uint2 *out = c.dst + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    if (lane > 0 && lane < 31) *reinterpret_cast<uint4 *>(out + wa) = make_uint4(nva, nha, nvb, nhb);
+    else if (lane == 0) out[wa + 1] = make_uint2(nvb, nhb);
+    else out[wa] = make_uint2(nva, nha);
 }
 
-// colour coin: BLACK iff u < 1/2  <=>  bit 63 of the draw is 0
-// (_kernels.py:44-45, sweeps.py:266-269)
-__device__ __forceinline__ int sweep_color(const SweepCtx &c, uint64_t gkey, uint64_t salt) {
-    return c.color_override >= 0 ? c.color_override : (int)(mix64(gkey + salt) >> 63);
-}
-
-// One sweep, one block per non-empty tile.
-template <int TM>
-__global__ void __launch_bounds__(32 * (kTileRows + 1))
-    domino_sweep_kernel(SweepCtx c) {
-    __shared__ uint2 fs[kTileRows + 1][32];
-    const int z = blockIdx.z;
-    const uint64_t step = c.step + (c.step_dev ? *c.step_dev : 0ull);
-    const uint64_t salt = (step + 1ull) * kGold;
-    const uint64_t base = c.seedinfo[2 * z];
-    const int color = sweep_color(c, c.seedinfo[2 * z + 1], salt);
-    sweep_tile<TM, false>(c, c.tiles[blockIdx.x], c.src + (size_t)z * c.chain_stride + c.pitch,
-                          c.dst + (size_t)z * c.chain_stride + c.pitch, base, salt, color, fs);
+// Colours of the next kGraphSweeps sweeps of every chain (graph mode).
+__global__ void colors_kernel(const uint64_t *seedinfo, const uint64_t *step_dev, uint64_t offset,
+                              uint8_t *colors) {
+    const int z = blockIdx.x, i = threadIdx.x;
+    const uint64_t step = *step_dev + offset + (uint64_t)i;
+    colors[z * kGraphSweeps + i] = (uint8_t)(mix64(seedinfo[2 * z + 1] + (step + 1ull) * kGold) >> 63);
 }
 
 // --------------------------------------------------------------- codecs
@@ -304,32 +328,38 @@ int push_seeds(tsb_domino *h, int n, const uint64_t *seeds) {
 int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override, cudaStream_t stream,
                  const uint64_t *step_dev) {
     SweepCtx c;
-    c.step_dev = step_dev;
-    c.src = h->buf[h->cur] + (size_t)chain0 * h->chain_stride;
-    c.dst = h->buf[h->cur ^ 1] + (size_t)chain0 * h->chain_stride;
-    c.range = h->range;
+    const size_t off = (size_t)chain0 * h->chain_stride + h->pitch + kPad;  // row 0, word 0
+    c.src = h->buf[h->cur] + off;
+    c.dst = h->buf[h->cur ^ 1] + off;
     c.seedinfo = h->seedinfo;
     c.tgrid = h->tgrid;
+    c.step_dev = step_dev;
+    c.colors = step_dev ? h->colors : nullptr;
+    c.tiles = h->tiles;
+    c.ntiles = h->ntiles;
     c.t0 = h->t0;
     c.t1 = h->t1;
     c.chain_stride = h->chain_stride;
     c.side = h->side;
-    c.W = h->W;
     c.pitch = h->pitch;
     c.step = step;
     c.color_override = color_override;
-    c.tiles = h->tiles;
-    c.ntiles = h->ntiles;
-    if (h->ntiles == 0) { h->cur ^= 1; return TSB_OK; }
-    dim3 grid(h->ntiles, 1, n);
-    dim3 block(32 * (kTileRows + 1));
-    switch (h->tmode) {
-        case 0: domino_sweep_kernel<0><<<grid, block, 0, stream>>>(c); break;
-        case 1: domino_sweep_kernel<1><<<grid, block, 0, stream>>>(c); break;
-        default: domino_sweep_kernel<2><<<grid, block, 0, stream>>>(c); break;
-    }
-    TSB_CUDA(cudaGetLastError());
     h->cur ^= 1;
+    if (h->ntiles == 0) return TSB_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->ntiles, 1, n);
+    cfg.blockDim = dim3(32 * (kTileRows + 1));
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    switch (h->tmode) {
+        case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_sweep_kernel<0>, c)); break;
+        case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_sweep_kernel<1>, c)); break;
+        default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_sweep_kernel<2>, c)); break;
+    }
     return TSB_OK;
 }
 
@@ -352,6 +382,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     cudaGraph_t g = nullptr;
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
+    colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
     for (int i = 0; i < kGraphSweeps && !rc; ++i)
         rc = launch_sweep(h, chain0, n, (uint64_t)i, -1, h->cap_stream, h->step_dev);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
@@ -404,7 +435,10 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     h->side = side;
     h->nchains = nchains;
     h->W = (side + 31) / 32;
-    h->pitch = (h->W + 31) / 32 * 32;  // 256-byte aligned rows
+    // rows: kPad zero words, W words, zero padding up to the last tile's halo;
+    // 256-byte aligned
+    const int nchunks_ = (h->W + 1 + kTileWords - 1) / kTileWords;
+    h->pitch = (kPad + nchunks_ * kTileWords + 2 + 31) / 32 * 32;
     h->chain_stride = (size_t)(side + 2) * h->pitch;
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaStreamCreate"); }
@@ -430,6 +464,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         return bail(e, "cudaMallocHost seeds");
     if ((e = cudaMalloc(&h->bad, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc flag");
     if ((e = cudaMalloc(&h->step_dev, sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
+    if ((e = cudaMalloc(&h->colors, (size_t)kGraphSweeps * nchains)) != cudaSuccess) return bail(e, "cudaMalloc colors");
     if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess)
         return bail(e, "cudaEventCreate");
     if ((e = cudaEventRecord(h->seed_ev, h->stream)) != cudaSuccess) return bail(e, "cudaEventRecord");
@@ -466,6 +501,12 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         }
     }
     h->ntiles = (int)tiles.size();
+    {
+        int per_sm = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, domino_sweep_kernel<2>, 32 * (kTileRows + 1), 0);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        h->sweep_blocks = std::max(1, per_sm * nsm);
+    }
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
         return bail(e, "cudaMalloc tiles");
     if (!tiles.empty() &&
@@ -490,6 +531,7 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->bytes);
     cudaFree(h->bad);
     cudaFree(h->step_dev);
+    cudaFree(h->colors);
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->seed_pinned) cudaFreeHost(h->seed_pinned);
@@ -553,7 +595,7 @@ int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states) {
     TSB_CUDA(cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
     pack_kernel<<<dim3((h->W + 127) / 128, h->side, n), 128, 0, h->stream>>>(
         h->bytes, h->side, h->W, h->pitch, h->chain_stride, h->dom,
-        h->buf[h->cur] + (size_t)chain0 * h->chain_stride, h->bad);
+        h->buf[h->cur] + (size_t)chain0 * h->chain_stride + kPad, h->bad);
     TSB_CUDA(cudaGetLastError());
     int bad = 0;
     TSB_CUDA(cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -571,7 +613,7 @@ int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states) {
     const size_t grid = (size_t)h->side * h->side;
     if ((rc = ensure_bytes(h, grid * n))) return rc;
     unpack_kernel<<<dim3((h->side + 127) / 128, h->side, n), 128, 0, h->stream>>>(
-        h->buf[h->cur] + (size_t)chain0 * h->chain_stride, h->side, h->pitch, h->chain_stride, h->bytes);
+        h->buf[h->cur] + (size_t)chain0 * h->chain_stride + kPad, h->side, h->pitch, h->chain_stride, h->bytes);
     TSB_CUDA(cudaGetLastError());
     TSB_CUDA(cudaMemcpyAsync(states, h->bytes, grid * n, cudaMemcpyDeviceToHost, h->stream));
     TSB_CUDA(cudaStreamSynchronize(h->stream));

@@ -13,6 +13,7 @@ struct tsb_domino {
     int2 *range = nullptr;
     int2 *tiles = nullptr;  // non-empty sweep tiles {word chunk, row band}
     int ntiles = 0;
+    int sweep_blocks = 1;  // resident blocks of the sweep kernel (grid-strided tile loop)
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;
@@ -26,6 +27,7 @@ struct tsb_domino {
     bool own_stream = false;
     // CUDA graph of kGraphSweeps sweeps, replayed by long walks
     uint64_t *step_dev = nullptr;
+    uint8_t *colors = nullptr;  // [nchains][kGraphSweeps] colours of the current replay
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
@@ -33,6 +35,7 @@ struct tsb_domino {
 };
 
 constexpr int kGraphSweeps = 32;
+constexpr int kStatePad = 2;  // == kPad in domino.cu: zero words left of every state row
 
 
 namespace tsb {

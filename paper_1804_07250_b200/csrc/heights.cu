@@ -237,7 +237,7 @@ int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *
     TSB_CUDA(cudaMalloc(&dout, nv * sizeof(int32_t)));
     TSB_CUDA(cudaMalloc(&dflags, 2 * sizeof(int)));
     bool overflow = false;
-    const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride;
+    const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride + kStatePad;
     int rc = relax<0>(h, dh, ref_r * h->side + ref_c, st, dflags, &overflow);
     int hf = 0;
     if (!rc && !overflow) {
@@ -284,7 +284,7 @@ int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, 
         cudaMemsetAsync(dflags, 0, 2 * sizeof(int), h->stream);
         finish_heights_kernel<<<dim3((h->side + 127) / 128, h->side), 128, 0, h->stream>>>(
             dh, h->dom, h->side, h->pitch, dout, pass == 0 ? kInf : -kInf, dflags);
-        uint2 *st = h->buf[h->cur] + (size_t)(pass == 0 ? chain_max : chain_min) * h->chain_stride;
+        uint2 *st = h->buf[h->cur] + (size_t)(pass == 0 ? chain_max : chain_min) * h->chain_stride + kStatePad;
         decode_extremal_kernel<<<dim3((h->W + 127) / 128, h->side), 128, 0, h->stream>>>(
             dout, h->dom, h->fbits, h->side, h->W, h->pitch, st, dflags + 1);
         cudaMemcpyAsync(hf, dflags, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream);
