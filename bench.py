@@ -7,12 +7,15 @@ Metric (BASELINE.json): flip attempts/s = in-domain sites of the active
 colour class per sweep x sweeps / time, on the Aztec diamond of order 4096
 (33,579,009 in-domain vertices), uniform weights, start T_max, seed 0x5EED.
 
-One "step" = `--sweeps-per-step` consecutive sweeps (default 100) of one
+One "step" = `--sweeps-per-step` consecutive sweeps (default 1000) of one
 chain; between timed steps L2 is flushed by writing a 256 MiB buffer
 (outside the events), each step timed with CUDA events on the launching
 stream, and the per-rank total is reduced with MAX over ranks.  With N > 1
-(torchrun) every rank runs an independent chain of the same lattice on its
-own GPU (replicas, weak scaling); rank 0 prints one JSON line.
+(torchrun) the one chain is strip-sharded over the GPUs (strong scaling):
+each rank sweeps its rows plus --halo halo rows and swaps halos with its
+neighbours over NCCL every --halo sweeps (paper_1804_07250_b200/strips.py);
+--replicas runs independent chains instead (weak scaling).  Rank 0 prints
+one JSON line.
 
 `--impl reference` times the reference algorithm's CPU path (the C port in
 oracle/, all host threads) on the same workload, rank 0 only.
@@ -46,9 +49,12 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--order", type=int, default=4096)
-    p.add_argument("--sweeps-per-step", type=int, default=100)
+    p.add_argument("--sweeps-per-step", type=int, default=1000)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--replicas", action="store_true",
+                   help="N>1: independent chains per GPU (weak scaling) instead of strip sharding")
+    p.add_argument("--halo", type=int, default=32, help="strip sharding: halo rows = sweeps between exchanges")
     return p.parse_args()
 
 
@@ -185,7 +191,8 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak",
+        "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": {"workload": f"aztec{args.order}_uniform_from_Tmax",
                                         "sweeps_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
@@ -219,13 +226,31 @@ def main():
     S = args.sweeps_per_step
     stream = torch.cuda.current_stream()
 
+    strips = world > 1 and not args.replicas
+    if strips:
+        seed = SEED  # one chain sharded over all GPUs
     h = DominoHandle(d, d.n + 1, 1)
     h.set_stream(stream.cuda_stream)
     h.set_p_up(plan.p_up)
     h.upload(t_max[None])
+    if strips:
+        from paper_1804_07250_b200.strips import DominoStripEngine, StripWalker, strip_bounds
+
+        bounds = strip_bounds(d.vertex_mask, world, min_rows=args.halo)
+        walker = StripWalker(None, bounds, rank, world, args.halo)
+        walker.engine = DominoStripEngine(h, walker.window)
+        strip_vertices = int(d.vertex_mask[walker.lo:walker.hi].sum())
+
+        def run(n, step0):
+            walker.walk(seed, n, step0=step0)
+    else:
+        def run(n, step0):
+            h.walk([seed], n, step0=step0)
+    clk = ClockSampler(local).__enter__()  # nvidia-smi needs ~0.5 s to start sampling
+    time.sleep(1.0)
     step = 0
     for _ in range(args.warmup):
-        h.walk([seed], S, step0=step)
+        run(S, step)
         step += S
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
@@ -233,14 +258,14 @@ def main():
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     first = step
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()  # evict L2 between timed steps (outside the events)
-            ev[k][0].record(stream)
-            h.walk([seed], S, step0=step)
-            ev[k][1].record(stream)
-            step += S
-        torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()  # evict L2 between timed steps (outside the events)
+        ev[k][0].record(stream)
+        run(S, step)
+        ev[k][1].record(stream)
+        step += S
+    torch.cuda.synchronize()
+    clk.__exit__()
     if world > 1:
         dist.barrier()
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -249,18 +274,44 @@ def main():
     a = torch.tensor([float(att)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(a, op=dist.ReduceOp.SUM)
+        if not strips:  # replicas: every rank ran its own chain
+            dist.all_reduce(a, op=dist.ReduceOp.SUM)
     max_ms = float(t.item())
     value = float(a.item()) / (max_ms / 1e3)
 
     # roofline of the dominant kernel (domino_sweep_kernel: one launch per sweep)
     n_domain = counts[0] + counts[1]
+    n_rank = strip_vertices if strips else n_domain
     per_launch_ms = total_ms / (args.steps * S)
-    achieved = n_domain / (per_launch_ms / 1e3) / 1e9  # 1 B/vertex/sweep algorithmic
+    achieved = n_rank / (per_launch_ms / 1e3) / 1e9  # 1 B/vertex/sweep algorithmic
     peak, peak_src = peaks()
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and strips:
+        import ctypes
+
+        rows = walker.hi - walker.lo
+        host = torch.empty(rows * walker.engine.row_bytes, dtype=torch.uint8, pin_memory=True)
+        seeds_h = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        seeds_d = torch.empty(1, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            seeds_h[0] = k
+            seeds_d.copy_(seeds_h, non_blocking=True)  # the step's input (its seed index)
+            run(S, step)
+            step += S
+            host.copy_(walker.engine.get_rows(walker.lo, rows), non_blocking=True)  # the step's result
+            torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e_att = attempts_for(seed, step - args.steps * S, args.steps * S, counts)
+        e2e = {"value": e2e_att / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": 8,
+               "d2h_bytes_per_step": int(host.numel()),
+               "api": "StripWalker over DominoHandle; state resident, strip rows read back to pinned host each step",
+               "clock": "host wall clock, max over ranks"}
+    if not args.no_e2e and not strips:
         t0_tiling = ts.Tiling(d, t_max)
         ts.random_walk(t0_tiling, seed, S, plan)  # warm the cached handle
         torch.cuda.synchronize()
@@ -290,16 +341,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic: Aztec diamond from the closed-form T_max, uniform weights",
             "config": {"workload": f"aztec{args.order}_uniform_from_Tmax", "order": args.order,
                        "domain_vertices": n_domain, "sweeps_per_step": S, "seed": SEED,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single chain",
+                       "parallelism": (f"strips x{world}, halo {args.halo} rows (NCCL p2p every {args.halo} sweeps)"
+                                       if strips else (f"replicas x{world}" if world > 1 else "single chain")),
                        "l2": "flushed (256 MiB write) between timed steps; state planes stay "
                              "L2-resident within a step by design"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "domino_sweep_kernel",
-                         "bytes_per_launch": n_domain, "peak_source": peak_src,
+                         "bytes_per_launch": n_rank, "peak_source": peak_src,
                          "accounting": "1 B per in-domain vertex per sweep (4-bit state read + write)"},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -91,6 +91,17 @@ int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, ui
                      int color);
 int tsb_domino_sync(tsb_domino *h);
 
+/* Strip sharding (multi-GPU): restrict sweeps to the tile bands
+ * covering rows [row_lo, row_hi) (row_hi < 0: all rows).  Rows outside the
+ * window are left untouched; a K-sweep walk keeps rows at distance >= K from
+ * the window edge exact (the dependency radius is one row per sweep). */
+int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi);
+/* Packed device rows for halo exchange: rows [r0, r0+nrows) of `chain`
+ * (r0 >= -1, -1 = guard row) copied to / from device memory, row_bytes each. */
+int tsb_domino_row_bytes(tsb_domino *h, int64_t *bytes);
+int tsb_domino_get_rows(tsb_domino *h, int chain, int r0, int nrows, void *dev_dst);
+int tsb_domino_set_rows(tsb_domino *h, int chain, int r0, int nrows, const void *dev_src);
+
 /* Height function of chain `chain` (lattice.py:537-580): int32 (side x side),
  * 0 outside Domain.vertex_mask, h(ref) = 0 at the reference vertex
  * (lattice.py:197-203).  TSB_E_INCONSISTENT when the state does not

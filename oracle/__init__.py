@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
         L.orc_uniform_from_key.argtypes = [_u64, _u64]
         L.orc_uniform_grid.argtypes = [_u64, ctypes.c_int, ctypes.c_int, _u64, _u64, _p]
         L.orc_domino_walk.argtypes = [_p, ctypes.c_int, ctypes.c_int, _p, _p, _u64, _u64, ctypes.c_int]
+        L.orc_domino_walk_window.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64, _p, _u64, _u64]
         L.orc_domino_sweep.argtypes = [_p, ctypes.c_int, _u64, _p, _u64, ctypes.c_int]
         L.orc_sv_walk.argtypes = [_p, ctypes.c_int, ctypes.c_int, _p, _p, _u64, _u64]
         L.orc_loz_walk.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p, _u64, _u64]
@@ -104,6 +105,14 @@ def domino_walk(states: np.ndarray, seeds, p_up: np.ndarray, n_steps: int,
     lib().orc_domino_walk(_ptr(out), out.shape[0], out.shape[-1], _ptr(seeds), _ptr(p),
                           step0, n_steps, threads)
     return out
+
+
+def domino_walk_window(rows: np.ndarray, row0: int, seed: int, p_up_rows: np.ndarray, n_steps: int,
+                       step0: int = 0) -> None:
+    """In place on a (nrows, V) window of rows [row0, row0+nrows)."""
+    assert rows.flags.c_contiguous and rows.dtype == np.uint8
+    p = np.ascontiguousarray(p_up_rows, dtype=np.float64)
+    lib().orc_domino_walk_window(_ptr(rows), rows.shape[0], rows.shape[1], row0, seed, _ptr(p), step0, n_steps)
 
 
 def domino_sweep(states: np.ndarray, seed: int, p_up: np.ndarray, step: int, color: int):

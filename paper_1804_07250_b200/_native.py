@@ -88,6 +88,10 @@ _SIGS = {
     "tsb_domino_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),
     "tsb_domino_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
     "tsb_domino_sync": (_i, [_vp]),
+    "tsb_domino_set_window": (_i, [_vp, _i, _i]),
+    "tsb_domino_row_bytes": (_i, [_vp, _vp]),
+    "tsb_domino_get_rows": (_i, [_vp, _i, _i, _i, _vp]),
+    "tsb_domino_set_rows": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_domino_walk_host": (_i, [_i, _vp, _i, _i, _vp, _vp, _vp, _u64]),
     "tsb_domino_heights": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_domino_extremal": (_i, [_vp, _i, _i, _i, _i]),

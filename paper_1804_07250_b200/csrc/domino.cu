@@ -335,8 +335,8 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     c.tgrid = h->tgrid;
     c.step_dev = step_dev;
     c.colors = step_dev ? h->colors : nullptr;
-    c.tiles = h->tiles;
-    c.ntiles = h->ntiles;
+    c.tiles = h->tiles + h->win_t0;
+    c.ntiles = h->win_tn;
     c.t0 = h->t0;
     c.t1 = h->t1;
     c.chain_stride = h->chain_stride;
@@ -347,7 +347,8 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     h->cur ^= 1;
     if (h->ntiles == 0) return TSB_OK;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(h->ntiles, 1, n);
+    if (h->win_tn == 0) return TSB_OK;
+    cfg.gridDim = dim3(h->win_tn, 1, n);
     cfg.blockDim = dim3(32 * (kTileRows + 1));
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -372,7 +373,8 @@ __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev
 // device memory).
 int ensure_graph(tsb_domino *h, int chain0, int n) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
-                      h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1;
+                      h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
+                      h->g_win0 == h->win_t0 && h->g_winn == h->win_tn;
     if (same) return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -404,6 +406,8 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_tmode = h->tmode;
     h->g_t0 = h->t0;
     h->g_t1 = h->t1;
+    h->g_win0 = h->win_t0;
+    h->g_winn = h->win_tn;
     return TSB_OK;
 }
 
@@ -501,6 +505,18 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         }
     }
     h->ntiles = (int)tiles.size();
+    h->win_t0 = 0;
+    h->win_tn = h->ntiles;
+    {
+        const int nb = (side + kTileRows - 1) / kTileRows;
+        h->band_start.assign(nb + 1, 0);
+        size_t i = 0;
+        for (int y = 0; y < nb; ++y) {
+            h->band_start[y] = (int)i;
+            while (i < tiles.size() && tiles[i].y == y) ++i;
+        }
+        h->band_start[nb] = (int)tiles.size();
+    }
     {
         int per_sm = 0, nsm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, domino_sweep_kernel<2>, 32 * (kTileRows + 1), 0);
@@ -628,7 +644,7 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
     uint64_t s = 0;
-    if (n_steps >= 2 * kGraphSweeps) {
+    if (n_steps >= kGraphSweeps) {
         if ((rc = ensure_graph(h, chain0, n))) return rc;
         set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
         TSB_CUDA(cudaGetLastError());
@@ -647,6 +663,48 @@ int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, ui
     if ((rc = push_seeds(h, n, seeds))) return rc;
     if ((rc = launch_sweep(h, chain0, n, step, color, h->stream, nullptr))) return rc;
     return settle(h, chain0, n, 1);
+}
+
+int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    if (row_hi < 0) row_hi = h->side;
+    row_lo = std::max(0, row_lo);
+    row_hi = std::min(h->side, row_hi);
+    if (row_hi <= row_lo) {
+        h->win_t0 = 0;
+        h->win_tn = 0;
+        return TSB_OK;
+    }
+    const int y0 = row_lo / kTileRows, y1 = (row_hi - 1) / kTileRows;
+    h->win_t0 = h->band_start[y0];
+    h->win_tn = h->band_start[y1 + 1] - h->win_t0;
+    return TSB_OK;
+}
+
+static int row_copy(tsb_domino *h, int chain, int r0, int nrows, void *dev, bool get) {
+    if (!h || !dev) return fail(TSB_E_VALUE, "null argument");
+    if (chain < 0 || chain >= h->nchains || r0 < -1 || nrows < 0 || r0 + nrows > h->side + 1)
+        return fail(TSB_E_VALUE, "rows [%d, %d) of chain %d out of range", r0, r0 + nrows, chain);
+    TSB_CUDA(cudaSetDevice(h->device));
+    uint2 *base = h->buf[h->cur] + (size_t)chain * h->chain_stride + (size_t)(r0 + 1) * h->pitch;
+    const size_t bytes = sizeof(uint2) * (size_t)nrows * h->pitch;
+    TSB_CUDA(cudaMemcpyAsync(get ? dev : (void *)base, get ? (const void *)base : dev, bytes, cudaMemcpyDeviceToDevice,
+                             h->stream));
+    return TSB_OK;
+}
+
+int tsb_domino_row_bytes(tsb_domino *h, int64_t *bytes) {
+    if (!h || !bytes) return fail(TSB_E_VALUE, "null argument");
+    *bytes = (int64_t)sizeof(uint2) * h->pitch;
+    return TSB_OK;
+}
+
+int tsb_domino_get_rows(tsb_domino *h, int chain, int r0, int nrows, void *dev_dst) {
+    return row_copy(h, chain, r0, nrows, dev_dst, true);
+}
+
+int tsb_domino_set_rows(tsb_domino *h, int chain, int r0, int nrows, const void *dev_src) {
+    return row_copy(h, chain, r0, nrows, const_cast<void *>(dev_src), false);
 }
 
 int tsb_domino_sync(tsb_domino *h) {

@@ -1,6 +1,8 @@
 // Domino handle shared by the domino translation units.
 #pragma once
 
+#include <vector>
+
 #include "tsb_internal.cuh"
 
 struct tsb_domino {
@@ -13,7 +15,9 @@ struct tsb_domino {
     int2 *range = nullptr;
     int2 *tiles = nullptr;  // non-empty sweep tiles {word chunk, row band}
     int ntiles = 0;
-    int sweep_blocks = 1;  // resident blocks of the sweep kernel (grid-strided tile loop)
+    int sweep_blocks = 1;      // resident blocks of the sweep kernel
+    std::vector<int> band_start;  // first tile of every row band (tiles are band-major)
+    int win_t0 = 0, win_tn = 0;   // swept tile range (row window; default all)
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;
@@ -32,6 +36,7 @@ struct tsb_domino {
     cudaGraphExec_t graph_exec = nullptr;
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
     uint64_t g_t0 = 0, g_t1 = 0;
+    int g_win0 = -1, g_winn = -1;
 };
 
 constexpr int kGraphSweeps = 32;

@@ -220,3 +220,41 @@ def test_cftp_batching_and_progress():
     trace = ts.CftpTrace()
     ts.cftp_sample(one, ts.SweepPlan(one), 9, trace=trace)
     assert trace.rounds == []
+
+
+def test_strip_windows_on_one_device():
+    """Two 'ranks' in one process: windowed walks + device row exchange
+    (the NCCL path of bench.py --gpus N without the network) reproduce the
+    single-handle walk."""
+    import torch
+
+    from paper_1804_07250_b200.strips import DominoStripEngine, StripWalker, strip_bounds
+
+    order, halo, steps = 300, 16, 150
+    d = ts.Domain.aztec(order)
+    t_max, _ = ts.lattice.aztec_extremal_states(order)
+    plan = ts.SweepPlan(d)
+    bounds = strip_bounds(d.vertex_mask, 2, min_rows=halo)
+    engines, walkers = [], []
+    for rank in range(2):
+        h = DominoHandle(d, d.n + 1, 1)
+        h.set_stream(torch.cuda.current_stream().cuda_stream)
+        h.set_p_up(plan.p_up)
+        h.upload(t_max[None])
+        w = StripWalker(None, bounds, rank, 2, halo)
+        w.engine = DominoStripEngine(h, w.window)
+        walkers.append(w)
+    s = 0
+    while s < steps:
+        k = min(halo, steps - s)
+        for w in walkers:
+            w.engine.walk(0x5EED, s, k)
+        a, b = walkers
+        up = a.engine.get_rows(a.hi - halo, halo)
+        dn = b.engine.get_rows(b.lo, halo)
+        b.engine.set_rows(b.lo - halo, halo, up)
+        a.engine.set_rows(a.hi, halo, dn)
+        s += k
+    full = ts.random_walk_batch(t_max[None], [0x5EED], steps, plan)[0]
+    got = np.concatenate([walkers[r].engine.h.download()[0][bounds[r]:bounds[r + 1]] for r in range(2)])
+    assert np.array_equal(got, full)

@@ -1,0 +1,57 @@
+"""Strip sharding with the CUDA engine: 2 processes share cuda:0 over gloo
+(host-staged rows; on a multi-GPU box the same walker runs over NCCL) and
+must reproduce the single-GPU walk bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ORDER, SEED, STEPS, HALO = 700, 0x5EED, 300, 24
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.strips import DominoStripEngine, StripWalker, strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    d = ts.Domain.aztec(ORDER)
+    t_max, _ = aztec_extremal_states(ORDER)
+    h = DominoHandle(d, d.n + 1, 1, device=0)
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.upload(t_max[None])
+    bounds = strip_bounds(d.vertex_mask, world, min_rows=HALO)
+    w = StripWalker(None, bounds, rank, world, HALO, stage_cpu=True)
+    w.engine = DominoStripEngine(h, w.window)
+    w.walk(SEED, STEPS)
+    np.save(os.path.join(out_dir, f"strip{rank}.npy"), h.download()[0][w.lo:w.hi])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strips_two_processes_one_gpu(tmp_path, world):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    d = ts.Domain.aztec(ORDER)
+    t_max, _ = aztec_extremal_states(ORDER)
+    ref = ts.random_walk_batch(t_max[None], [SEED], STEPS, ts.SweepPlan(d))[0]
+    got = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
+    assert np.array_equal(got, ref)
