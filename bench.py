@@ -76,6 +76,15 @@ def attempts_for(seed: int, step0: int, n: int, counts) -> int:
     return sum(counts[rng.color_at(seed, s)] for s in range(step0, step0 + n))
 
 
+def traffic(kernel: str):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return int(json.load(f)[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -350,7 +359,9 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps; state planes stay "
                              "L2-resident within a step by design"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "domino_sweep_kernel",
+                         "frac": achieved / peak, "traffic": traffic("domino_sweep_kernel"),
+                         "traffic_source": "profiles/traffic.json (ncu --set full capture)",
+                         "kernel": "domino_sweep_kernel",
                          "bytes_per_launch": n_rank, "peak_source": peak_src,
                          "accounting": "1 B per in-domain vertex per sweep (4-bit state read + write)"},
             "cpu_baseline": cpu,

@@ -11,9 +11,8 @@ pinned against golden vectors produced by the Python reference itself
 (tests/golden/make_golden.py -> tests/golden/*.npz, checked by
 tests/test_oracle_golden.py).
 
-`heights.py` restates the height/extremal integrators in numpy for small
-sizes (reference `lattice.py:537-754`, `lozenge.py:414-775`,
-`sixvertex.py:247-562`).
+Heights and extremal states are checked directly against the reference's
+own outputs stored in tests/golden/ (they are unique fixpoints).
 """
 
 from __future__ import annotations

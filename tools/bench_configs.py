@@ -1,0 +1,156 @@
+#!/usr/bin/env python
+"""Throughput of the BASELINE.json configs other than the headline metric
+(reported in DESIGN.md; bench.py is the contract line).  Device-resident
+states, CUDA-event timing on the handle's stream after warm-up.
+
+    python tools/bench_configs.py [--only c1,c2,c3,c5] [--quick]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(torch, stream, fn):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 1e3
+
+
+def c1(torch, stream, quick):
+    import hashlib
+
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200 import rng
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    d = ts.Domain.aztec(64)
+    t_max, _ = aztec_extremal_states(64)
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.upload(t_max[None])
+    h.walk([0x5EED], 1000)
+    fp = hashlib.sha256(h.download()[0].tobytes()).hexdigest()[:16]
+    h.upload(t_max[None])
+    dt = timed(torch, stream, lambda: h.walk([0x5EED], 1000))
+    mask = d.vertex_mask
+    par = np.add.outer(np.arange(d.n + 1), np.arange(d.n + 1)) & 1
+    counts = (int((mask & (par == 0)).sum()), int((mask & (par == 1)).sum()))
+    att = sum(counts[rng.color_at(0x5EED, s)] for s in range(1000))
+    return {"config": "C1 aztec64 T_max 1000 sweeps seed 0x5EED", "fingerprint": fp,
+            "seconds": dt, "us_per_sweep": dt * 1e3, "attempts_per_s": att / dt}
+
+
+def c2(torch, stream, quick):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lozenge import LozengeHandle, loz_p_up_grid
+
+    a = 300 if quick else 1000
+    d = ts.TriDomain.hexagon(a, a, a)
+    t0 = time.perf_counter()
+    t_max, t_min = ts.loz_extremal(d)
+    t_ext = time.perf_counter() - t0
+    w = ts.VolumeWeights(0.999)
+    h = LozengeHandle(d, 1)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(loz_p_up_grid(d, w))
+    h.upload(t_min.edges[None])
+    steps = 10_000
+    h.walk([0x5EED], 320)
+    dt = timed(torch, stream, lambda: h.walk([0x5EED], steps, step0=320))
+    nv = int(d.vertex_mask.sum())
+    return {"config": f"C2 lozenge hexagon {a},{a},{a} VolumeWeights(0.999) from T_min, {steps} sweeps",
+            "extremal_s": t_ext, "us_per_sweep": dt / steps * 1e6, "attempts_per_s": nv / 3 * steps / dt,
+            "domain_vertices": nv}
+
+
+def c3(torch, stream, quick):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.sixvertex import SixVertexHandle
+
+    n = 512 if quick else 2048
+    t0 = time.perf_counter()
+    hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+    t_ext = time.perf_counter() - t0
+    out = []
+    for w, label in (((1.0, 1.0, 1.0), "Delta=1/2 (disordered)"), ((1.0, 1.0, math.sqrt(8.0)), "Delta=-3 (antiferroelectric)")):
+        h = SixVertexHandle(n, 1)
+        h.set_stream(stream.cuda_stream)
+        h.set_weights(ts.SVWeights(*w))
+        h.upload(lo.heights[None])
+        steps = 10_000
+        h.walk([0x5EED], 200)
+        dt = timed(torch, stream, lambda: h.walk([0x5EED], steps, step0=200))
+        faces = (n - 1) ** 2
+        out.append({"config": f"C3 six-vertex DWBC n={n} {label} from h_min, {steps} sweeps",
+                    "extremal_s": t_ext, "us_per_sweep": dt / steps * 1e6,
+                    "attempts_per_s": faces / 4 * steps / dt})
+    return out
+
+
+def c5(torch, stream, quick):
+    """CFTP order 512: time the first rounds of a 64-sample batch (a full
+    sample needs ~21 rounds); reports coupled chain-sweeps per second."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.cftp import chain_master_seed
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+    import ctypes
+
+    from paper_1804_07250_b200 import _native
+
+    order, count, rounds = (128, 16, 8) if quick else (512, 64, 10)
+    d = ts.Domain.aztec(order)
+    t_max, t_min = aztec_extremal_states(order)
+    h = DominoHandle(d, d.n + 1, 2 * count + 2)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    masters = np.array([chain_master_seed(0x5EED, k) for k in range(count)], dtype=np.uint64)
+    out = np.zeros((count, d.n + 1, d.n + 1), dtype=np.uint8)
+    rr = np.zeros(count, dtype=np.int32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc = _native.lib().tsb_domino_cftp(h._h, _native.ptr(t_max), _native.ptr(t_min), _native.ptr(masters), count,
+                                       rounds, _native.ptr(out), _native.ptr(rr), None, None)
+    dt = time.perf_counter() - t0
+    chain_sweeps = 2 * count * sum(2 ** (r + 1) - 2 for r in range(1, rounds + 1))
+    return {"config": f"C5 CFTP aztec {order}, {count} samples, first {rounds} rounds",
+            "status": "coalesced" if rc == 0 else "cap (expected: not all samples coalesce this early)",
+            "collapsed": int((rr > 0).sum()), "seconds": dt, "chain_sweeps": chain_sweeps,
+            "chain_sweeps_per_s": chain_sweeps / dt,
+            "attempts_per_s": chain_sweeps * int(d.vertex_mask.sum()) / 2 / dt}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--only", default="c1,c2,c3,c5")
+    p.add_argument("--quick", action="store_true")
+    args = p.parse_args()
+    import torch
+
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    for name in args.only.split(","):
+        r = globals()[name](torch, stream, args.quick)
+        for x in r if isinstance(r, list) else [r]:
+            print(json.dumps(x), flush=True)
+
+
+if __name__ == "__main__":
+    main()
