@@ -33,6 +33,10 @@ namespace tsb {
 constexpr int kTileRows = 15;   // output rows per block tile (+1 halo fire row)
 constexpr int kTileWords = 62;  // output words per tile: 64 loaded (2 per lane), 1 halo word each side
 constexpr int kPad = 2;         // zero words left of every state row (lane 0's halo of the first tile)
+constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
+constexpr int kMK = 2;          // sweeps per temporally blocked launch
+constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
+constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
     const uint2 *src;          // chain 0, row 0, word 0 (after the kPad left pad)
@@ -191,6 +195,80 @@ __global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
     if (lane > 0 && lane < 31) *reinterpret_cast<uint4 *>(out + wa) = make_uint4(nva, nha, nvb, nhb);
     else if (lane == 0) out[wa + 1] = make_uint2(nvb, nhb);
     else out[wa] = make_uint2(nva, nha);
+}
+
+// Temporal blocking: kMK sweeps per launch.  A block holds kMRows rows
+// (warp k owns row r0 - kMK + k, two words per lane as above) entirely in
+// registers/shared memory and sweeps them kMK times; rows and halo words next
+// to the unloaded outside go stale by one row / bit per sweep, so after kMK
+// sweeps the central kMOut rows and the 62 interior words are exact and are
+// the only ones stored.  Per sweep it costs two block barriers and the fire
+// test; loads, stores, addressing and the launch are paid once per kMK sweeps.
+// Used inside the graph replays (colours from the per-replay table).
+template <int TM>
+__global__ void __launch_bounds__(32 * kMRows, 2) domino_multi_kernel(SweepCtx c) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint2(*vs)[32] = reinterpret_cast<uint2(*)[32]>(dsm);
+    uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
+    uint32_t(*fres)[64] = reinterpret_cast<uint32_t(*)[64]>(dsm + 2 * sizeof(uint2) * kMRows * 32);
+    uint16_t(*queue)[1024] =
+        reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64);
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
+    const int r = tile.y * kMOut - kMK + k;
+    const int wa = tile.x * kTileWords - 2 + 2 * lane;
+    const int z = blockIdx.z;
+    const bool in_grid = r >= 0 && r < c.side;
+    const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint4 cur = make_uint4(0u, 0u, 0u, 0u);
+    if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
+    const uint64_t step0 = *c.step_dev + c.step;
+#pragma unroll 1
+    for (int s = 0; s < kMK; ++s) {
+        const uint64_t step = step0 + (uint64_t)s;
+        const int color = c.colors[z * kGraphSweeps + (int)c.step + s];
+        vs[k][lane] = make_uint2(cur.x, cur.z);
+        __syncthreads();
+        uint32_t vua = 0u, vub = 0u;
+        if (k > 0) {
+            const uint2 u = vs[k - 1][lane];
+            vua = u.x;
+            vub = u.y;
+        }
+        const uint32_t act = ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u;
+        uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
+        if (lane == 0) hl = 0u;
+        const uint32_t la = (cur.y << 1) | (hl >> 31);
+        const uint32_t ia = vua & cur.x & ~(la | cur.y);
+        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act;
+        const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
+        const uint32_t ib = vub & cur.z & ~(lb | cur.w);
+        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act;
+        uint2 f = make_uint2(0u, 0u);
+        if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
+            const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
+            f = warp_fire<TM>(ra, rb, ia, ib, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step);
+        }
+        fs[k][lane] = f;
+        __syncthreads();
+        const uint2 fn = k + 1 < kMRows ? fs[k + 1][lane] : make_uint2(0u, 0u);  // F(r+1)
+        uint32_t frb = __shfl_down_sync(0xffffffffu, f.x, 1);
+        if (lane == 31) frb = 0u;
+        const uint32_t nva = cur.x ^ f.x ^ fn.x;
+        const uint32_t nvb = cur.z ^ f.y ^ fn.y;
+        const uint32_t nha = cur.y ^ f.x ^ (f.x >> 1) ^ (f.y << 31);
+        const uint32_t nhb = cur.w ^ f.y ^ (f.y >> 1) ^ (frb << 31);
+        cur = in_grid ? make_uint4(nva, nha, nvb, nhb) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (k >= kMK && k < kMRows - kMK && in_grid) {  // warp-uniform
+        uint2 *out = c.dst + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+        if (lane > 0 && lane < 31) *reinterpret_cast<uint4 *>(out + wa) = cur;
+        else if (lane == 0) out[wa + 1] = make_uint2(cur.z, cur.w);
+        else out[wa] = make_uint2(cur.x, cur.y);
+    }
 }
 
 // Colours of the next kGraphSweeps sweeps of every chain (graph mode).
@@ -364,6 +442,45 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     return TSB_OK;
 }
 
+// kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
+int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream_t stream) {
+    SweepCtx c;
+    const size_t off = (size_t)chain0 * h->chain_stride + h->pitch + kPad;
+    c.src = h->buf[h->cur] + off;
+    c.dst = h->buf[h->cur ^ 1] + off;
+    c.seedinfo = h->seedinfo;
+    c.tgrid = h->tgrid;
+    c.step_dev = h->step_dev;
+    c.colors = h->colors;
+    c.tiles = h->mtiles + h->win_m0;
+    c.ntiles = h->win_mn;
+    c.t0 = h->t0;
+    c.t1 = h->t1;
+    c.chain_stride = h->chain_stride;
+    c.side = h->side;
+    c.pitch = h->pitch;
+    c.step = step_off;
+    c.color_override = -1;
+    h->cur ^= 1;
+    if (h->win_mn == 0) return TSB_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->win_mn, 1, n);
+    cfg.blockDim = dim3(32 * kMRows);
+    cfg.dynamicSmemBytes = kMSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    switch (h->tmode) {
+        case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<0>, c)); break;
+        case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<1>, c)); break;
+        default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<2>, c)); break;
+    }
+    return TSB_OK;
+}
+
 __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
 __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
 
@@ -374,7 +491,7 @@ __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev
 int ensure_graph(tsb_domino *h, int chain0, int n) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
                       h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
-                      h->g_win0 == h->win_t0 && h->g_winn == h->win_tn;
+                      h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0;
     if (same) return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -385,8 +502,8 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
     colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
-    for (int i = 0; i < kGraphSweeps && !rc; ++i)
-        rc = launch_sweep(h, chain0, n, (uint64_t)i, -1, h->cap_stream, h->step_dev);
+    static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
+    for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) {
@@ -408,13 +525,14 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_t1 = h->t1;
     h->g_win0 = h->win_t0;
     h->g_winn = h->win_tn;
+    h->g_winm = h->win_m0;
     return TSB_OK;
 }
 
 // After an odd number of sweeps the walked chains live in the other buffer;
 // copy them back so the handle keeps one canonical buffer for all chains.
-int settle(tsb_domino *h, int chain0, int n, uint64_t nsweeps) {
-    if ((nsweeps & 1) == 0 || n == h->nchains) return TSB_OK;
+int settle(tsb_domino *h, int chain0, int n, int cur0) {
+    if (h->cur == cur0 || n == h->nchains) return TSB_OK;
     const size_t off = (size_t)chain0 * h->chain_stride;
     TSB_CUDA(cudaMemcpyAsync(h->buf[h->cur ^ 1] + off, h->buf[h->cur] + off,
                              sizeof(uint2) * h->chain_stride * n, cudaMemcpyDeviceToDevice, h->stream));
@@ -493,36 +611,42 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     std::vector<int2> rg(side);
     if ((e = cudaMemcpy(rg.data(), h->range, sizeof(int2) * side, cudaMemcpyDeviceToHost)) != cudaSuccess)
         return bail(e, "ranges");
-    std::vector<int2> tiles;
     const int nchunks = (h->W + 1 + kTileWords - 1) / kTileWords;
-    for (int y = 0; y * kTileRows < side; ++y) {
-        int lo = INT_MAX, hi = INT_MIN;
-        for (int r = y * kTileRows; r < std::min(side, (y + 1) * kTileRows); ++r)
-            if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
-        for (int x = 0; x < nchunks; ++x) {
-            const int w0 = x * kTileWords - 1;
-            if (hi > w0 && lo < w0 + kTileWords) tiles.push_back(make_int2(x, y));
+    // non-empty tiles of `band` output rows x kTileWords output words,
+    // band-major, plus the first tile of every band (row windows)
+    auto make_tiles = [&](int band, std::vector<int2> &tl, std::vector<int> &bstart) {
+        const int nb = (side + band - 1) / band;
+        bstart.assign(nb + 1, 0);
+        for (int y = 0; y < nb; ++y) {
+            bstart[y] = (int)tl.size();
+            int lo = INT_MAX, hi = INT_MIN;
+            for (int r = y * band; r < std::min(side, (y + 1) * band); ++r)
+                if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
+            for (int x = 0; x < nchunks; ++x) {
+                const int w0 = x * kTileWords - 1;
+                if (hi > w0 && lo < w0 + kTileWords) tl.push_back(make_int2(x, y));
+            }
         }
-    }
+        bstart[nb] = (int)tl.size();
+    };
+    std::vector<int2> tiles, mtiles;
+    make_tiles(kTileRows, tiles, h->band_start);
+    make_tiles(kMOut, mtiles, h->mband_start);
     h->ntiles = (int)tiles.size();
+    h->nmtiles = (int)mtiles.size();
     h->win_t0 = 0;
     h->win_tn = h->ntiles;
-    {
-        const int nb = (side + kTileRows - 1) / kTileRows;
-        h->band_start.assign(nb + 1, 0);
-        size_t i = 0;
-        for (int y = 0; y < nb; ++y) {
-            h->band_start[y] = (int)i;
-            while (i < tiles.size() && tiles[i].y == y) ++i;
-        }
-        h->band_start[nb] = (int)tiles.size();
-    }
-    {
-        int per_sm = 0, nsm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, domino_sweep_kernel<2>, 32 * (kTileRows + 1), 0);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-        h->sweep_blocks = std::max(1, per_sm * nsm);
-    }
+    h->win_m0 = 0;
+    h->win_mn = h->nmtiles;
+    if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mtiles.size()))) != cudaSuccess)
+        return bail(e, "cudaMalloc mtiles");
+    if (!mtiles.empty() &&
+        (e = cudaMemcpy(h->mtiles, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(e, "mtiles");
+    for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
+                           (const void *)domino_multi_kernel<2>})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem)) != cudaSuccess)
+            return bail(e, "smem attribute");
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
         return bail(e, "cudaMalloc tiles");
     if (!tiles.empty() &&
@@ -542,6 +666,7 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->fbits);
     cudaFree(h->range);
     cudaFree(h->tiles);
+    cudaFree(h->mtiles);
     cudaFree(h->tgrid);
     cudaFree(h->seedinfo);
     cudaFree(h->bytes);
@@ -643,6 +768,7 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
     if (!seeds) return fail(TSB_E_VALUE, "null seeds");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
+    const int cur0 = h->cur;
     uint64_t s = 0;
     if (n_steps >= kGraphSweeps) {
         if ((rc = ensure_graph(h, chain0, n))) return rc;
@@ -652,7 +778,7 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
     }
     for (; s < n_steps; ++s)
         if ((rc = launch_sweep(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;
-    return settle(h, chain0, n, n_steps);
+    return settle(h, chain0, n, cur0);
 }
 
 int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int color) {
@@ -661,8 +787,9 @@ int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, ui
     if (color != 0 && color != 1) return fail(TSB_E_VALUE, "colour must be 0 (BLACK) or 1 (WHITE)");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
+    const int cur0 = h->cur;
     if ((rc = launch_sweep(h, chain0, n, step, color, h->stream, nullptr))) return rc;
-    return settle(h, chain0, n, 1);
+    return settle(h, chain0, n, cur0);
 }
 
 int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi) {
@@ -671,13 +798,16 @@ int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi) {
     row_lo = std::max(0, row_lo);
     row_hi = std::min(h->side, row_hi);
     if (row_hi <= row_lo) {
-        h->win_t0 = 0;
-        h->win_tn = 0;
+        h->win_t0 = h->win_tn = h->win_m0 = h->win_mn = 0;
         return TSB_OK;
     }
-    const int y0 = row_lo / kTileRows, y1 = (row_hi - 1) / kTileRows;
+    int y0 = row_lo / kTileRows, y1 = (row_hi - 1) / kTileRows;
     h->win_t0 = h->band_start[y0];
     h->win_tn = h->band_start[y1 + 1] - h->win_t0;
+    y0 = row_lo / kMOut;
+    y1 = (row_hi - 1) / kMOut;
+    h->win_m0 = h->mband_start[y0];
+    h->win_mn = h->mband_start[y1 + 1] - h->win_m0;
     return TSB_OK;
 }
 

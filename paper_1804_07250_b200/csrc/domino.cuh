@@ -15,9 +15,12 @@ struct tsb_domino {
     int2 *range = nullptr;
     int2 *tiles = nullptr;  // non-empty sweep tiles {word chunk, row band}
     int ntiles = 0;
-    int sweep_blocks = 1;      // resident blocks of the sweep kernel
     std::vector<int> band_start;  // first tile of every row band (tiles are band-major)
     int win_t0 = 0, win_tn = 0;   // swept tile range (row window; default all)
+    int2 *mtiles = nullptr;       // tiles of the temporally blocked kernel (kMOut-row bands)
+    int nmtiles = 0;
+    std::vector<int> mband_start;
+    int win_m0 = 0, win_mn = 0;
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;
@@ -36,7 +39,7 @@ struct tsb_domino {
     cudaGraphExec_t graph_exec = nullptr;
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
     uint64_t g_t0 = 0, g_t1 = 0;
-    int g_win0 = -1, g_winn = -1;
+    int g_win0 = -1, g_winn = -1, g_winm = -1;
 };
 
 constexpr int kGraphSweeps = 32;
@@ -49,5 +52,5 @@ int check_range(tsb_domino *h, int chain0, int n);
 int push_seeds(tsb_domino *h, int n, const uint64_t *seeds);
 int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override, cudaStream_t stream,
                  const uint64_t *step_dev);
-int settle(tsb_domino *h, int chain0, int n, uint64_t nsweeps);
+int settle(tsb_domino *h, int chain0, int n, int cur0);
 }  // namespace tsb
