@@ -25,6 +25,7 @@
 // patches and passes p_high, converted here to exact integer thresholds.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "tsb_internal.cuh"
@@ -43,6 +44,15 @@ struct tsb_sv {
     int *flag = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // temporally blocked walks (sv_multi_kernel) replayed from a CUDA graph
+    uint32_t *bits2 = nullptr;  // second buffer (out-of-place launches)
+    uint64_t *step_dev = nullptr;
+    int m_wpl = 1, m_nw = 8, m_K = 4, m_out = 8, m_stride = 32, m_woff = 0, m_gx = 1, m_gy = 1;
+    size_t m_smem = 0;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int g_chain0 = -1, g_n = -1;
+    uint64_t lut_version = 0, g_lut_version = ~0ull;
 };
 
 namespace tsb {
@@ -133,6 +143,234 @@ __global__ void __launch_bounds__(256) sv_sweep_kernel(SvCtx c) {
     const uint32_t flip = sv_rng(cand, is_min, dnw, dne, dsw, dse, (uint64_t)R * (uint64_t)c.f, w, base, salt, c.lut);
     if (flip) rc[w] = b ^ flip;
 }
+
+// ---------------------------------------------------------------------------
+// Temporal blocking: K class sweeps per launch (sv_multi_kernel).
+//
+// A block of NW warps holds a tile of 2*NW rows x 32*WPL words in registers
+// (warp k owns tile rows 2k and 2k+1; lane l owns words l*WPL .. l*WPL+WPL-1)
+// with a shared-memory copy of every row for the vertical neighbours.  In a
+// sweep of class (pr, pc) every warp updates exactly one of its rows (the one
+// with R % 2 == pr) and reads only rows of the other parity, which no warp
+// writes in that sweep, so one block barrier per sweep suffices.  Rows and
+// words next to the unloaded outside go stale by one row / bit per sweep, so
+// after K sweeps the central 2*NW - 2K rows (and, for tiles with word halos,
+// all but the first and last word) are exact and are the only ones stored.
+// Out of place (double buffer): neighbouring tiles read each other's rows.
+// Class coins, site coins and the heat-bath LUT are exactly those of
+// sv_sweep_kernel, so the result is bit-identical for any tiling.
+struct SvMCtx {
+    const uint32_t *src;  // chain 0, row 0 (after the guard row)
+    uint32_t *dst;
+    const int32_t *h00;
+    const uint64_t *seedinfo;
+    const uint64_t *step_dev;
+    size_t chain_words;
+    int n, f, W, pitch;
+    int K, out_rows;      // sweeps per launch, exact rows per tile (2*NW - 2K)
+    int stride, woff;     // column tiles: first word of tile x = x*stride + woff
+    uint64_t step;        // offset of this launch inside the graph replay
+    uint64_t lut[32];
+};
+
+template <int WPL, int NW>
+constexpr size_t sv_multi_smem() {
+    return sizeof(uint32_t) * (2 * NW) * (32 * WPL)    // rows
+           + sizeof(uint64_t) * 32                      // lut
+           + sizeof(uint32_t) * NW * (32 * WPL)         // per-warp flip words
+           + sizeof(uint32_t) * NW * (32 * WPL) * 16;   // per-warp job queues
+}
+
+template <int WPL, int NW>
+__global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
+    constexpr int TW = 32 * WPL, TR = 2 * NW;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t(*rows)[TW] = reinterpret_cast<uint32_t(*)[TW]>(dsm);
+    uint64_t *lut = reinterpret_cast<uint64_t *>(dsm + sizeof(uint32_t) * TR * TW);
+    uint32_t *fres = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32) +
+                     (threadIdx.x >> 5) * TW;
+    uint32_t *queue = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32 +
+                                                   sizeof(uint32_t) * NW * TW) +
+                      (threadIdx.x >> 5) * TW * 16;
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const int z = blockIdx.z;
+    const int r0 = (int)blockIdx.y * c.out_rows - c.K;  // even
+    const int wl = (int)blockIdx.x * c.stride + c.woff + lane * WPL;  // first word of this lane
+    if (threadIdx.x < 32) lut[threadIdx.x] = c.lut[threadIdx.x];
+    const uint64_t base = c.seedinfo[2 * z], gkey = c.seedinfo[2 * z + 1];
+    const int p0 = c.h00[z] & 1;
+    // interior columns 1..n-1 of this lane's words
+    uint32_t cm[WPL];
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+        const int w = wl + j, c0 = w * 32;
+        uint32_t m = (w >= 0 && w < c.W) ? 0xFFFFFFFFu : 0u;
+        if (c0 < 1) m &= ~1u;
+        const int hi = c.n - 1 - c0;
+        if (hi < 31) m &= hi < 0 ? 0u : (0xFFFFFFFFu >> (31 - hi));
+        cm[j] = m;
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t step0 = *c.step_dev + c.step;
+    // class of sweep s is computed by lane s: min(int(u*4),3) = x >> 62
+    const int mycls = (int)(mix64(gkey + (step0 + (uint64_t)lane + 1ull) * kGold) >> 62);
+    const uint32_t *src = c.src + (size_t)z * c.chain_words;
+    const int Ra = r0 + 2 * k;
+    uint32_t ra[WPL], rb[WPL];  // rows Ra, Ra + 1
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+        const int w = wl + j;
+        const bool inw = w >= 0 && w < c.W;
+        ra[j] = (inw && Ra >= 0 && Ra < c.f) ? __ldcg(src + (size_t)Ra * c.pitch + w) : 0u;
+        rb[j] = (inw && Ra + 1 >= 0 && Ra + 1 < c.f) ? __ldcg(src + (size_t)(Ra + 1) * c.pitch + w) : 0u;
+        rows[2 * k][lane * WPL + j] = ra[j];
+        rows[2 * k + 1][lane * WPL + j] = rb[j];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int s = 0; s < c.K; ++s) {
+        const int cls = __shfl_sync(0xffffffffu, mycls, s);
+        const int pr = cls >> 1, pc = cls & 1;
+        const int i = 2 * k + pr, R = r0 + i;
+        uint32_t u[WPL], b[WPL], d[WPL];
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+            if (pr == 0) {
+                b[j] = ra[j];
+                d[j] = rb[j];
+                u[j] = i > 0 ? rows[i - 1][lane * WPL + j] : 0u;
+            } else {
+                b[j] = rb[j];
+                u[j] = ra[j];
+                d[j] = i + 1 < TR ? rows[i + 1][lane * WPL + j] : 0u;
+            }
+        }
+        uint32_t uL = __shfl_up_sync(0xffffffffu, u[WPL - 1], 1), bL = __shfl_up_sync(0xffffffffu, b[WPL - 1], 1),
+                 dL = __shfl_up_sync(0xffffffffu, d[WPL - 1], 1);
+        uint32_t uR = __shfl_down_sync(0xffffffffu, u[0], 1), bR = __shfl_down_sync(0xffffffffu, b[0], 1),
+                 dR = __shfl_down_sync(0xffffffffu, d[0], 1);
+        if (lane == 0) uL = bL = dL = 0u;
+        if (lane == 31) uR = bR = dR = 0u;
+        const bool rowok = R >= 1 && R <= c.n - 1;
+        const int odd = (pr + pc + p0) & 1;  // parity of the class faces
+        const uint32_t pcm = pc ? 0xAAAAAAAAu : 0x55555555u;
+        uint32_t mn[WPL], cand[WPL], nw[WPL], ne[WPL], sw[WPL], se[WPL];
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+            const uint32_t pb = j > 0 ? b[j - 1] : bL, nb = j < WPL - 1 ? b[j + 1] : bR;
+            const uint32_t pu = j > 0 ? u[j - 1] : uL, nu = j < WPL - 1 ? u[j + 1] : uR;
+            const uint32_t pd = j > 0 ? d[j - 1] : dL, nd = j < WPL - 1 ? d[j + 1] : dR;
+            const uint32_t left = (b[j] << 1) | (pb >> 31), right = (b[j] >> 1) | (nb << 31);
+            const uint32_t eq_u = ~(u[j] ^ b[j]), eq_d = ~(d[j] ^ b[j]), eq_l = ~(left ^ b[j]),
+                           eq_r = ~(right ^ b[j]);
+            const uint32_t all_eq = eq_u & eq_d & eq_l & eq_r, all_ne = ~(eq_u | eq_d | eq_l | eq_r);
+            const uint32_t act = rowok ? (cm[j] & pcm) : 0u;
+            mn[j] = (odd ? all_ne : all_eq) & act;
+            cand[j] = mn[j] | ((odd ? all_eq : all_ne) & act);
+            nw[j] = ((u[j] << 1) | (pu >> 31)) ^ b[j];
+            ne[j] = ((u[j] >> 1) | (nu << 31)) ^ b[j];
+            sw[j] = ((d[j] << 1) | (pd >> 31)) ^ b[j];
+            se[j] = ((d[j] >> 1) | (nd << 31)) ^ b[j];
+            cnt += __popc(cand[j]);
+        }
+        const int maxc = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+        if (maxc != 0 && maxc <= 4) {
+            // sparse: every lane draws its own candidates, two chains at a time
+            const uint64_t salt = (step0 + (uint64_t)s + 1ull) * kGold;
+            const uint64_t row_idx = (uint64_t)R * (uint64_t)c.f;
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+                uint32_t m = cand[j], fl = 0u;
+                const uint64_t widx = row_idx + (uint64_t)(int64_t)((wl + j) * 32);
+                while (m) {
+                    const int b0 = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int b1 = m ? __ffs(m) - 1 : b0;
+                    m &= m - 1;
+                    const uint64_t x0 = mix64(mix64(base + (widx + (uint64_t)b0 + 1ull) * kGold) + salt);
+                    const uint64_t x1 = mix64(mix64(base + (widx + (uint64_t)b1 + 1ull) * kGold) + salt);
+                    const uint32_t li0 = (((mn[j] >> b0) & 1u) ? 0u : 16u) | (((nw[j] >> b0) & 1u) << 3) |
+                                         (((ne[j] >> b0) & 1u) << 2) | (((sw[j] >> b0) & 1u) << 1) | ((se[j] >> b0) & 1u);
+                    const uint32_t li1 = (((mn[j] >> b1) & 1u) ? 0u : 16u) | (((nw[j] >> b1) & 1u) << 3) |
+                                         (((ne[j] >> b1) & 1u) << 2) | (((sw[j] >> b1) & 1u) << 1) | ((se[j] >> b1) & 1u);
+                    if (((x0 >> 11) < lut[li0]) == !(li0 & 16u)) fl |= 1u << b0;
+                    if (((x1 >> 11) < lut[li1]) == !(li1 & 16u)) fl |= 1u << b1;
+                }
+                if (fl) {
+                    const uint32_t nb = b[j] ^ fl;
+                    if (pr == 0) ra[j] = nb;
+                    else rb[j] = nb;
+                    rows[i][lane * WPL + j] = nb;
+                }
+            }
+        } else if (maxc != 0) {
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            int pos = incl - cnt;
+            // job = li << 12 | lane << 7 | j << 5 | bit;  li = (up ? 0 : 16) | nw<<3 | ne<<2 | sw<<1 | se
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+                for (uint32_t m = cand[j]; m; m &= m - 1) {
+                    const int bt = __ffs(m) - 1;
+                    const uint32_t li = (((mn[j] >> bt) & 1u) ? 0u : 16u) | (((nw[j] >> bt) & 1u) << 3) |
+                                        (((ne[j] >> bt) & 1u) << 2) | (((sw[j] >> bt) & 1u) << 1) |
+                                        ((se[j] >> bt) & 1u);
+                    queue[pos++] = (li << 12) | ((uint32_t)lane << 7) | ((uint32_t)j << 5) | (uint32_t)bt;
+                }
+                fres[lane * WPL + j] = 0u;
+            }
+            __syncwarp();
+            const uint64_t salt = (step0 + (uint64_t)s + 1ull) * kGold;
+            // site index R * f + 32 * (word) + bit, word = wl(lane 0) + lane' * WPL + j
+            const uint64_t row_idx = (uint64_t)R * (uint64_t)c.f + (uint64_t)(int64_t)((wl - lane * WPL) * 32);
+            for (int q = lane; q < total; q += 64) {
+                const bool two = q + 32 < total;
+                const uint32_t j0 = queue[q], j1 = two ? queue[q + 32] : j0;
+                const uint64_t i0 = row_idx + (uint64_t)((((j0 >> 7) & 31u) * WPL + ((j0 >> 5) & 3u)) * 32u + (j0 & 31u));
+                const uint64_t i1 = row_idx + (uint64_t)((((j1 >> 7) & 31u) * WPL + ((j1 >> 5) & 3u)) * 32u + (j1 & 31u));
+                const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
+                const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
+                // local min (up) moves iff u < p_high; local max moves iff u >= p_high
+                if (((x0 >> 11) < lut[j0 >> 12]) == !((j0 >> 16) & 1u))
+                    atomicOr(&fres[((j0 >> 7) & 31u) * WPL + ((j0 >> 5) & 3u)], 1u << (j0 & 31u));
+                if (two && ((x1 >> 11) < lut[j1 >> 12]) == !((j1 >> 16) & 1u))
+                    atomicOr(&fres[((j1 >> 7) & 31u) * WPL + ((j1 >> 5) & 3u)], 1u << (j1 & 31u));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+                const uint32_t nb = b[j] ^ fres[lane * WPL + j];
+                if (pr == 0) ra[j] = nb;
+                else rb[j] = nb;
+                rows[i][lane * WPL + j] = nb;
+            }
+        }
+        __syncthreads();
+    }
+    // store the exact rows / words
+    uint32_t *dst = c.dst + (size_t)z * c.chain_words;
+    const bool halo = c.woff < 0;
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+        const int w = wl + j;
+        bool ok = w >= 0 && w < c.W;
+        if (halo && ((lane == 0 && j == 0) || (lane == 31 && j == WPL - 1))) ok = false;
+        if (!ok) continue;
+        if (2 * k >= c.K && 2 * k < TR - c.K && Ra < c.f && Ra >= 0) dst[(size_t)Ra * c.pitch + w] = ra[j];
+        if (2 * k + 1 >= c.K && 2 * k + 1 < TR - c.K && Ra + 1 < c.f && Ra + 1 >= 0)
+            dst[(size_t)(Ra + 1) * c.pitch + w] = rb[j];
+    }
+}
+
+__global__ void sv_set_step(uint64_t *p, uint64_t v) { *p = v; }
+__global__ void sv_advance_step(uint64_t *p, uint64_t by) { *p += by; }
 
 // int32 heights (count, f, f) -> bits; validates |dh| == 1 across every edge.
 __global__ void sv_pack_kernel(const int32_t *h, int f, int W, int pitch, size_t chain_words, uint32_t *bits,
@@ -266,6 +504,130 @@ __global__ void __launch_bounds__(256) sv_coalesced_kernel(const uint32_t *bits,
     if (threadIdx.x == 0) flags[j] = (any || h00[chain0 + 2 * j] != h00[chain0 + 2 * j + 1]) ? 0 : 1;
 }
 
+constexpr int kSvGraphSweeps = 32;  // sweeps per graph replay
+
+// Tile geometry of sv_multi_kernel: rows of W <= 128 words fit one column
+// tile (WPL = ceil(W/32) words per lane, no word halo); wider grids use
+// 4 words per lane with a one-word halo on each side.  K sweeps per launch
+// (even, dividing kSvGraphSweeps with an even number of launches per replay)
+// and NW warps per block; TSB_SV_K / TSB_SV_NW override them for tuning.
+void sv_multi_config(tsb_sv *h) {
+    int force = 0;
+    if (const char *e = getenv("TSB_SV_WPL")) force = atoi(e);
+    if (force >= 1 && force <= 4) {
+        h->m_wpl = force;
+        h->m_woff = -1;
+        h->m_stride = 32 * force - 2;
+        h->m_gx = (h->W + h->m_stride - 1) / h->m_stride;
+    } else if (h->W <= 128) {
+        h->m_wpl = (h->W + 31) / 32;
+        h->m_woff = 0;
+        h->m_stride = 32 * h->m_wpl;
+        h->m_gx = 1;
+    } else {
+        h->m_wpl = 4;
+        h->m_woff = -1;
+        h->m_stride = 32 * 4 - 2;
+        h->m_gx = (h->W + h->m_stride - 1) / h->m_stride;
+    }
+    int nw = 16, K = 8;
+    if (const char *e = getenv("TSB_SV_NW")) nw = atoi(e) == 16 ? 16 : 8;
+    if (const char *e = getenv("TSB_SV_K")) K = atoi(e);
+    if (K != 2 && K != 4 && K != 8 && K != 16) K = 4;
+    while (2 * nw - 2 * K < 2) K /= 2;
+    h->m_nw = nw;
+    h->m_K = K;
+    h->m_out = 2 * nw - 2 * K;
+    h->m_gy = (h->f + h->m_out - 1) / h->m_out;
+}
+
+template <int WPL, int NW>
+static int sv_launch_multi_t(const cudaLaunchConfig_t &cfg0, const SvMCtx &c) {
+    constexpr size_t smem = sv_multi_smem<WPL, NW>();
+    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = cfg0;
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = smem;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW>, c));
+    return TSB_OK;
+}
+
+// One temporally blocked launch (m_K sweeps) of chains [chain0, chain0+n).
+static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, const uint32_t *src, uint32_t *dst,
+                           cudaStream_t stream) {
+    SvMCtx c;
+    c.src = src + (size_t)chain0 * h->chain_words + h->pitch;
+    c.dst = dst + (size_t)chain0 * h->chain_words + h->pitch;
+    c.h00 = h->h00 + chain0;
+    c.seedinfo = h->seedinfo;
+    c.step_dev = h->step_dev;
+    c.chain_words = h->chain_words;
+    c.n = h->n;
+    c.f = h->f;
+    c.W = h->W;
+    c.pitch = h->pitch;
+    c.K = h->m_K;
+    c.out_rows = h->m_out;
+    c.stride = h->m_stride;
+    c.woff = h->m_woff;
+    c.step = step_off;
+    for (int i = 0; i < 32; ++i) c.lut[i] = h->lut[i];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->m_gx, h->m_gy, n);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int key = h->m_wpl * 100 + h->m_nw;
+    switch (key) {
+        case 108: return sv_launch_multi_t<1, 8>(cfg, c);
+        case 208: return sv_launch_multi_t<2, 8>(cfg, c);
+        case 308: return sv_launch_multi_t<3, 8>(cfg, c);
+        case 408: return sv_launch_multi_t<4, 8>(cfg, c);
+        case 116: return sv_launch_multi_t<1, 16>(cfg, c);
+        case 216: return sv_launch_multi_t<2, 16>(cfg, c);
+        case 316: return sv_launch_multi_t<3, 16>(cfg, c);
+        default: return sv_launch_multi_t<4, 16>(cfg, c);
+    }
+}
+
+// Graph of kSvGraphSweeps sweeps: an even number of out-of-place launches
+// (bits -> bits2 -> bits ...), then step += kSvGraphSweeps.
+static int sv_ensure_graph(tsb_sv *h, int chain0, int n) {
+    if (h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_lut_version == h->lut_version) return TSB_OK;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    if (!h->cap_stream) TSB_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = TSB_OK;
+    const int launches = kSvGraphSweeps / h->m_K;
+    for (int i = 0; i < launches && !rc; ++i)
+        rc = sv_launch_multi(h, chain0, n, (uint64_t)i * h->m_K, (i & 1) ? h->bits2 : h->bits,
+                             (i & 1) ? h->bits : h->bits2, h->cap_stream);
+    sv_advance_step<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kSvGraphSweeps);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "sv graph capture");
+    e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        h->graph_exec = nullptr;
+        return cuda_fail(e, "sv graph instantiate");
+    }
+    h->g_chain0 = chain0;
+    h->g_n = n;
+    h->g_lut_version = h->lut_version;
+    return TSB_OK;
+}
+
 int sv_check(tsb_sv *h, int chain0, int n) {
     if (!h) return fail(TSB_E_VALUE, "null handle");
     if (chain0 < 0 || n < 0 || chain0 + n > h->nchains)
@@ -338,7 +700,11 @@ int tsb_sv_create(int device, int n, int nchains, tsb_sv **out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->flag, sizeof(int));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(h->seed_ev, h->stream);
+    if (e == cudaSuccess) e = cudaMalloc(&h->bits2, sizeof(uint32_t) * h->chain_words * nchains);
+    if (e == cudaSuccess) e = cudaMemset(h->bits2, 0, sizeof(uint32_t) * h->chain_words * nchains);
+    if (e == cudaSuccess) e = cudaMalloc(&h->step_dev, sizeof(uint64_t));
     for (int i = 0; i < 32; ++i) h->lut[i] = 1ull << 52;
+    sv_multi_config(h);
     if (e != cudaSuccess) {
         int code = cuda_fail(e, "tsb_sv_create");
         tsb_sv_destroy(h);
@@ -357,6 +723,10 @@ int tsb_sv_destroy(tsb_sv *h) {
     cudaFree(h->seedinfo);
     cudaFree(h->hbuf);
     cudaFree(h->flag);
+    cudaFree(h->bits2);
+    cudaFree(h->step_dev);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->seed_pinned) cudaFreeHost(h->seed_pinned);
     if (h->seed_ev) cudaEventDestroy(h->seed_ev);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -377,6 +747,7 @@ int tsb_sv_set_stream(tsb_sv *h, void *stream) {
 int tsb_sv_set_p_high(tsb_sv *h, const double *p_high) {
     if (!h || !p_high) return fail(TSB_E_VALUE, "null argument");
     for (int i = 0; i < 32; ++i) h->lut[i] = threshold_of(p_high[i]);
+    ++h->lut_version;
     return TSB_OK;
 }
 
@@ -432,7 +803,15 @@ static int sv_walk_impl(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uin
     const int class_rows = (h->f + 1) / 2;
     const int warps = 8;
     dim3 grid((h->W + 31) / 32, (class_rows + warps - 1) / warps, n);
-    for (uint64_t s = 0; s < n_steps; ++s) {
+    uint64_t done = 0;
+    const uint64_t replays = class_override < 0 ? n_steps / kSvGraphSweeps : 0;
+    if (replays) {
+        if ((rc = sv_ensure_graph(h, chain0, n))) return rc;
+        sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        for (uint64_t r = 0; r < replays; ++r) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
+        done = replays * kSvGraphSweeps;
+    }
+    for (uint64_t s = done; s < n_steps; ++s) {
         c.step = step0 + s;
         sv_sweep_kernel<<<grid, 32 * warps, 0, h->stream>>>(c);
     }

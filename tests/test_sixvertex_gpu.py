@@ -98,3 +98,42 @@ def test_sweep_stays_monotone_coupled():
     hi, lo = closed_form(n)
     out = sv_random_walk_batch(np.stack([hi, lo]).astype(np.int32), [9, 9], 300, ts.SVWeights(1, 1, 1.5))
     assert (out[0] >= out[1]).all()
+
+
+@pytest.mark.parametrize("n,steps", [(1100, 70), (2048, 40), (3500, 36), (4200, 34)])
+def test_multi_tile_geometries(n, steps):
+    """Temporally blocked graph replays at every tile width (1..4 words per
+    lane, and the word-halo tiling beyond 128 words per row) vs the oracle."""
+    hi, lo = closed_form(n)
+    start = np.stack([lo, hi]).astype(np.int32)
+    seeds = np.array([0x5EED, 77], dtype=np.uint64)
+    weights = ts.SVWeights(1.0, 1.0, math.sqrt(8.0))
+    h = SixVertexHandle(n, 2)
+    h.set_weights(weights)
+    h.upload(start)
+    # a warm-up that leaves the state mixed near the corners, then the test walk
+    h.walk(seeds, steps)
+    mid = h.download()
+    ref_mid = oracle.sv_walk(start, seeds, weights.table(), steps)
+    assert np.array_equal(mid, ref_mid)
+
+
+@pytest.mark.parametrize("K,NW,WPL,n", [(2, 8, 0, 300), (4, 8, 0, 300), (8, 16, 0, 300), (16, 16, 0, 300),
+                                        (4, 16, 0, 300), (8, 16, 1, 300), (8, 16, 1, 1500), (4, 8, 2, 1500),
+                                        (8, 16, 3, 1500)])
+def test_multi_k_nw(monkeypatch, K, NW, WPL, n):
+    """Every sweeps-per-launch / block-height / tile-width setting is bit-identical."""
+    monkeypatch.setenv("TSB_SV_K", str(K))
+    monkeypatch.setenv("TSB_SV_NW", str(NW))
+    monkeypatch.setenv("TSB_SV_WPL", str(WPL))
+    steps = 150 if n < 1000 else 70
+    hi, lo = closed_form(n)
+    start = np.stack([lo, hi, lo]).astype(np.int32)
+    seeds = np.array([5, 6, 2**64 - 1], dtype=np.uint64)
+    weights = ts.SVWeights(0.7, 1.2, 1.5)
+    h = SixVertexHandle(n, 3)
+    h.set_weights(weights)
+    h.upload(start)
+    h.walk(seeds, 70)
+    h.walk(seeds, steps - 70, step0=70)
+    assert np.array_equal(h.download(), oracle.sv_walk(start, seeds, weights.table(), steps))
