@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "domino.cuh"
+#include "tsb_fire.cuh"
 
 namespace tsb {
 
@@ -53,62 +54,6 @@ struct SweepCtx {
     uint64_t step;
     int color_override;  // -1: colour from the global coin (direct launches)
 };
-
-// Heat-bath coins of a warp's rotateable active vertices, load-balanced.
-// Each lane owns two words (bits `ra`, `rb` rotateable; `ia`, `ib`: state 3).
-// The warp's sites are queued in shared memory and dealt round-robin to the
-// lanes, two independent splitmix64 chains per lane per iteration, so a word
-// full of rotateable sites no longer serialises its lane (dense mixed states).
-// A site moves 3 -> 12 when u < p_up and 12 -> 3 otherwise
-// (_kernels.py:49-55, sweeps.py:102-110); only rotateable sites are drawn and
-// counter-based draws make the skipping exact.
-template <int TM>
-__device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, uint32_t ib, uint16_t *queue,
-                                        uint32_t *fres, const uint64_t *__restrict__ seedinfo,
-                                        const uint64_t *__restrict__ tgrid, uint64_t t, int side, int z, int r,
-                                        int wa, uint64_t step) {
-    const int lane = threadIdx.x & 31;
-    const int cnt = __popc(ra) + __popc(rb);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int pos = incl - cnt;
-    // job = is3 << 11 | lane << 6 | word << 5 | bit
-    for (uint32_t m = ra; m; m &= m - 1) {
-        const int b = __ffs(m) - 1;
-        queue[pos++] = (uint16_t)((((ia >> b) & 1u) << 11) | (lane << 6) | b);
-    }
-    for (uint32_t m = rb; m; m &= m - 1) {
-        const int b = __ffs(m) - 1;
-        queue[pos++] = (uint16_t)((((ib >> b) & 1u) << 11) | (lane << 6) | 32 | b);
-    }
-    fres[2 * lane] = 0u;
-    fres[2 * lane + 1] = 0u;
-    __syncwarp();
-    const uint64_t base = seedinfo[2 * z];
-    const uint64_t salt = (step + 1ull) * kGold;
-    // site index r * side + column; column = 32 * (wa of lane 0) + 64 * lane + 32 * word + bit
-    const uint64_t row_idx = (uint64_t)r * (uint64_t)side + (uint64_t)(int64_t)((wa - 2 * lane) * 32);
-    for (int j = lane; j < total; j += 64) {
-        const bool two = j + 32 < total;
-        const uint32_t q0 = queue[j], q1 = two ? queue[j + 32] : q0;
-        const uint64_t i0 = row_idx + (uint64_t)(q0 & 63u) + (uint64_t)(((q0 >> 6) & 31u) * 64u);
-        const uint64_t i1 = row_idx + (uint64_t)(q1 & 63u) + (uint64_t)(((q1 >> 6) & 31u) * 64u);
-        // two independent chains for ILP
-        const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
-        const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
-        const uint64_t t0 = TM == 2 ? __ldg(tgrid + i0) : t;
-        const uint64_t t1 = TM == 2 ? __ldg(tgrid + i1) : t;
-        if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
-        if (two && ((x1 >> 11) < t1) == (bool)(q1 >> 11)) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
-    }
-    __syncwarp();
-    return make_uint2(fres[2 * lane], fres[2 * lane + 1]);
-}
 
 // One sweep, one block per non-empty tile of kTileRows x 62 words (512
 // threads).  Warp k owns row r = r0+k; each lane owns two adjacent words

@@ -18,14 +18,18 @@
 //   A[x] ^= F[x] ^ F[x+1];  B[x] ^= F[x] ^ F[x] >> 1;  C[x] ^= F[x] ^ F[x+1] << 1.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
-#include "tsb_internal.cuh"
+#include "tsb_fire.cuh"
 
 namespace tsb {
 constexpr int kLzRows = 15;   // output rows per tile (+1 halo fire row)
 constexpr int kLzWords = 62;  // output words per tile
 constexpr int kLzGraph = 32;  // sweeps per CUDA graph
+constexpr int kLzMRows = 16;  // rows per temporally blocked tile (warps per block)
+constexpr size_t kLzMSmem = sizeof(uint4) * kLzMRows * 32 + sizeof(uint2) * kLzMRows * 32 +
+                            sizeof(uint32_t) * kLzMRows * 64 + sizeof(uint16_t) * kLzMRows * 1024;
 }  // namespace tsb
 
 struct tsb_loz {
@@ -55,6 +59,9 @@ struct tsb_loz {
     cudaGraphExec_t graph_exec = nullptr;
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
     uint64_t g_t0 = 0;
+    int2 *mtiles = nullptr;  // tiles of the temporally blocked kernel (m_out-row bands)
+    int nmtiles = 0;
+    int m_K = 4, m_out = 8;
 };
 
 namespace tsb {
@@ -180,6 +187,109 @@ __global__ void __launch_bounds__(32 * (kLzRows + 1)) loz_sweep_kernel(LzCtx c) 
     } else {
         if (sa) { oA[wa] = nAa; oB[wa] = nBa; oC[wa] = nCa; }
         if (sb) { oA[wb] = nAb; oB[wb] = nBb; oC[wb] = nCb; }
+    }
+}
+
+struct LzMCtx {
+    const uint32_t *src;  // chain 0, plane A, row 0
+    uint32_t *dst;
+    const int2 *tiles;
+    const uint64_t *seedinfo;
+    const uint64_t *tgrid;
+    const uint64_t *step_dev;
+    uint64_t t0;
+    size_t plane, chain_words;
+    int X, Y, W, pitch;
+    int K, out_rows;
+    uint64_t step;  // offset of this launch inside the graph replay
+};
+
+// Temporal blocking: K sweeps per launch (graph replays), the domino
+// multi-sweep scheme on three planes.  Warp k owns row x0 - K + k, lane owns
+// words (wa, wa+1) of A, B and C in registers; per sweep the A/C words go to
+// shared memory for the row below (d2, d3), the fire words for the row above
+// (pull-form updates).  Rows / bits next to the unloaded outside go stale by
+// one per sweep, so the central kLzMRows - 2K rows and the 62 interior words
+// are exact and are the only ones stored.  Coins exactly as loz_sweep_kernel.
+template <int TM>
+__global__ void __launch_bounds__(32 * kLzMRows, 2) lz_multi_kernel(LzMCtx c) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint4(*acs)[32] = reinterpret_cast<uint4(*)[32]>(dsm);
+    uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint4) * kLzMRows * 32);
+    uint32_t(*fres)[64] =
+        reinterpret_cast<uint32_t(*)[64]>(dsm + sizeof(uint4) * kLzMRows * 32 + sizeof(uint2) * kLzMRows * 32);
+    uint16_t(*queue)[1024] = reinterpret_cast<uint16_t(*)[1024]>(
+        dsm + sizeof(uint4) * kLzMRows * 32 + sizeof(uint2) * kLzMRows * 32 + sizeof(uint32_t) * kLzMRows * 64);
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
+    const int x = tile.y * c.out_rows - c.K + k;
+    const int wa = tile.x * kLzWords - 2 + 2 * lane, wb = wa + 1;
+    const int z = blockIdx.z;
+    const uint64_t gkey = c.seedinfo[2 * z + 1];
+    const bool in_grid = x >= 0 && x < c.X;
+    const bool ina = in_grid && wa >= 0 && wa < c.pitch, inb = in_grid && wb >= 0 && wb < c.pitch;
+    // class residues: y = 32w + b == x - cls (mod 3), 32 == 2 (mod 3)
+    const int b3a = (((x - 2 * wa) % 3) + 3) % 3, b3b = (((x - 2 * wb) % 3) + 3) % 3;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t *rA = c.src + (size_t)z * c.chain_words + (ptrdiff_t)x * c.pitch;
+    const uint32_t *rB = rA + c.plane, *rC = rB + c.plane;
+    Words2 A = ld2(rA, wa, ina, inb), B = ld2(rB, wa, ina, inb), C = ld2(rC, wa, ina, inb);
+    const uint64_t step0 = *c.step_dev + c.step;
+    int mycls;
+    {
+        const double coin = (double)(mix64(gkey + (step0 + (uint64_t)lane + 1ull) * kGold) >> 11) * 0x1p-53;
+        mycls = min((int)__dmul_rn(coin, 3.0), 2);  // min(int(coin * 3), 2)
+    }
+#pragma unroll 1
+    for (int s = 0; s < c.K; ++s) {
+        const int cls = __shfl_sync(0xffffffffu, mycls, s);
+        acs[k][lane] = make_uint4(A.a, A.b, C.a, C.b);
+        __syncthreads();
+        const uint4 m = k > 0 ? acs[k - 1][lane] : make_uint4(0u, 0u, 0u, 0u);  // A, C of row x-1
+        uint32_t bprev = __shfl_up_sync(0xffffffffu, B.b, 1);
+        uint32_t cmnext = __shfl_down_sync(0xffffffffu, m.z, 1);
+        if (lane == 0) bprev = 0u;
+        if (lane == 31) cmnext = 0u;
+        const uint32_t d2a = (m.z >> 1) | (m.w << 31), d2b = (m.w >> 1) | (cmnext << 31);
+        const uint32_t d4a = (B.a << 1) | (bprev >> 31), d4b = (B.b << 1) | (B.a >> 31);
+        const uint32_t lowa = B.a & m.x & C.a & ~A.a & ~d2a & ~d4a, lowb = B.b & m.y & C.b & ~A.b & ~d2b & ~d4b;
+        const uint32_t higha = A.a & d2a & d4a & ~B.a & ~m.x & ~C.a, highb = A.b & d2b & d4b & ~B.b & ~m.y & ~C.b;
+        const uint32_t rota = (lowa | higha) & mod3_mask((b3a - cls + 3) % 3);
+        const uint32_t rotb = (lowb | highb) & mod3_mask((b3b - cls + 3) % 3);
+        uint2 f = make_uint2(0u, 0u);
+        if (__any_sync(0xffffffffu, (rota | rotb) != 0u))
+            f = warp_fire<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
+                              step0 + (uint64_t)s);
+        fs[k][lane] = f;
+        __syncthreads();
+        const uint2 fn = k + 1 < kLzMRows ? fs[k + 1][lane] : make_uint2(0u, 0u);  // F[x+1]
+        uint32_t fnprev = __shfl_up_sync(0xffffffffu, fn.y, 1);
+        uint32_t fnext = __shfl_down_sync(0xffffffffu, f.x, 1);
+        if (lane == 0) fnprev = 0u;
+        if (lane == 31) fnext = 0u;
+        if (in_grid) {
+            A.a ^= f.x ^ fn.x;
+            A.b ^= f.y ^ fn.y;
+            B.a ^= f.x ^ ((f.x >> 1) | (f.y << 31));
+            B.b ^= f.y ^ ((f.y >> 1) | (fnext << 31));
+            C.a ^= f.x ^ ((fn.x << 1) | (fnprev >> 31));
+            C.b ^= f.y ^ ((fn.y << 1) | (fn.x >> 31));
+        }
+    }
+    if (k >= c.K && k < kLzMRows - c.K && in_grid) {  // warp-uniform
+        uint32_t *oA = c.dst + (size_t)z * c.chain_words + (ptrdiff_t)x * c.pitch;
+        uint32_t *oB = oA + c.plane, *oC = oB + c.plane;
+        const bool sa = lane > 0 && wa >= 0 && wa < c.W, sb = lane < 31 && wb >= 0 && wb < c.W;
+        if (sa && sb) {
+            *reinterpret_cast<uint2 *>(oA + wa) = make_uint2(A.a, A.b);
+            *reinterpret_cast<uint2 *>(oB + wa) = make_uint2(B.a, B.b);
+            *reinterpret_cast<uint2 *>(oC + wa) = make_uint2(C.a, C.b);
+        } else {
+            if (sa) { oA[wa] = A.a; oB[wa] = B.a; oC[wa] = C.a; }
+            if (sb) { oA[wb] = A.b; oB[wb] = B.b; oC[wb] = C.b; }
+        }
     }
 }
 
@@ -514,6 +624,42 @@ int lz_launch(tsb_loz *h, int chain0, int n, uint64_t step, int cls, cudaStream_
     return TSB_OK;
 }
 
+// One temporally blocked launch (m_K sweeps); graph mode only.
+int lz_launch_multi(tsb_loz *h, int chain0, int n, uint64_t step_off, cudaStream_t stream) {
+    LzMCtx c;
+    c.src = h->buf[h->cur] + (size_t)chain0 * h->chain_words + h->pitch;
+    c.dst = h->buf[h->cur ^ 1] + (size_t)chain0 * h->chain_words + h->pitch;
+    c.tiles = h->mtiles;
+    c.seedinfo = h->seedinfo;
+    c.tgrid = h->tgrid;
+    c.step_dev = h->step_dev;
+    c.t0 = h->t0;
+    c.plane = h->plane;
+    c.chain_words = h->chain_words;
+    c.X = h->X;
+    c.Y = h->Y;
+    c.W = h->W;
+    c.pitch = h->pitch;
+    c.K = h->m_K;
+    c.out_rows = h->m_out;
+    c.step = step_off;
+    h->cur ^= 1;
+    if (h->nmtiles == 0) return TSB_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->nmtiles, 1, n);
+    cfg.blockDim = dim3(32 * kLzMRows);
+    cfg.dynamicSmemBytes = kLzMSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (h->tmode == 0) TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<0>, c));
+    else TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<2>, c));
+    return TSB_OK;
+}
+
 int lz_graph(tsb_loz *h, int chain0, int n) {
     if (h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur && h->g_tmode == h->tmode &&
         h->g_t0 == h->t0)
@@ -526,7 +672,9 @@ int lz_graph(tsb_loz *h, int chain0, int n) {
     cudaGraph_t g = nullptr;
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
-    for (int i = 0; i < kLzGraph && !rc; ++i) rc = lz_launch(h, chain0, n, (uint64_t)i, -1, h->cap_stream, h->step_dev);
+    // kLzGraph / m_K launches (even, so the buffers end where they started)
+    for (int i = 0; i < kLzGraph / h->m_K && !rc; ++i)
+        rc = lz_launch_multi(h, chain0, n, (uint64_t)i * h->m_K, h->cap_stream);
     lz_advance_step<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kLzGraph);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) {
@@ -647,6 +795,34 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
         return bail(e, "tiles");
     if (!tiles.empty()) cudaMemcpy(h->tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice);
+    // temporally blocked tiles: K sweeps per launch (TSB_LZ_K overrides; K | kLzGraph, even launch count)
+    {
+        int K = 4;
+        if (const char *ev = getenv("TSB_LZ_K")) K = atoi(ev);
+        if (K != 2 && K != 4 && K != 8 && K != 16) K = 4;
+        while (kLzMRows - 2 * K < 2) K /= 2;
+        h->m_K = K;
+        h->m_out = kLzMRows - 2 * K;
+        std::vector<int2> mt;
+        for (int y = 0; y * h->m_out < h->X; ++y) {
+            int lo = INT_MAX, hi = INT_MIN;
+            for (int x = y * h->m_out; x < std::min(h->X, (y + 1) * h->m_out); ++x)
+                if (rg[x].y > rg[x].x) { lo = std::min(lo, rg[x].x); hi = std::max(hi, rg[x].y); }
+            for (int cx = 0; cx < nchunks; ++cx) {
+                const int w0 = cx * kLzWords - 1;
+                if (hi > w0 && lo < w0 + kLzWords) mt.push_back(make_int2(cx, y));
+            }
+        }
+        h->nmtiles = (int)mt.size();
+        if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mt.size()))) != cudaSuccess)
+            return bail(e, "tiles");
+        if (!mt.empty()) cudaMemcpy(h->mtiles, mt.data(), sizeof(int2) * mt.size(), cudaMemcpyHostToDevice);
+        if ((e = cudaFuncSetAttribute(lz_multi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kLzMSmem)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(lz_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kLzMSmem)) != cudaSuccess)
+            return bail(e, "smem attribute");
+    }
     if ((e = cudaMalloc(&h->seedinfo, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess) return bail(e, "seeds");
     if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess) return bail(e, "seeds");
     if ((e = cudaMalloc(&h->flag, 2 * sizeof(int))) != cudaSuccess) return bail(e, "flag");
@@ -668,6 +844,7 @@ int tsb_loz_destroy(tsb_loz *h) {
     cudaFree(h->tri);
     cudaFree(h->range);
     cudaFree(h->tiles);
+    cudaFree(h->mtiles);
     cudaFree(h->tgrid);
     cudaFree(h->seedinfo);
     cudaFree(h->bytes);

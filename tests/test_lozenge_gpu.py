@@ -101,3 +101,22 @@ def test_monotone_coupling():
     h_lo = ts.loz_heights(ts.LozengeTiling(d, out[1])).heights
     m = d.vertex_mask
     assert (h_hi[m] >= h_lo[m]).all()
+
+
+@pytest.mark.parametrize("K", [2, 4, 8])
+@pytest.mark.parametrize("abc,w,steps", [((40, 50, 60), ts.VolumeWeights(0.95), 200),
+                                         ((700, 900, 800), ts.Uniform(), 70),
+                                         ((60, 20, 45), ts.LozEdgeWeights(1.0, {(("up", 30, 14), ("down", 30, 13)): 3.0}), 130)])
+def test_multi_sweep_vs_oracle(monkeypatch, K, abc, w, steps):
+    """Temporally blocked graph replays (K sweeps per launch) are bit-identical."""
+    monkeypatch.setenv("TSB_LZ_K", str(K))
+    d = ts.TriDomain.hexagon(*abc)
+    t_max, t_min = ts.loz_extremal(d)
+    start = np.stack([t_min.edges, t_max.edges])
+    seeds = np.array([0x5EED, 2**64 - 5], dtype=np.uint64)
+    p = loz_p_up_grid(d, w)
+    h = LozengeHandle(d, 2)
+    h.set_p_up(p)
+    h.upload(start)
+    h.walk(seeds, steps)
+    assert np.array_equal(h.download(), oracle.loz_walk(start, seeds, p, steps))
