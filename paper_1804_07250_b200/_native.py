@@ -146,13 +146,14 @@ def lib() -> ctypes.CDLL:
         return _lib
     with _lock:
         if _lib is None:
-            if _stale():
+            path = os.environ.get("TSB_LIB")  # A/B experiments: load another build of the same ABI
+            if path is None and _stale():
                 try:
                     build()
                 except (OSError, subprocess.CalledProcessError) as exc:
                     if not os.path.exists(LIB_PATH):
                         raise RuntimeError(f"libtsb.so is missing and could not be built: {exc}")
-            L = ctypes.CDLL(LIB_PATH)
+            L = ctypes.CDLL(path or LIB_PATH)
             for name, (res, args) in _SIGS.items():
                 fn = getattr(L, name)
                 fn.restype = res
