@@ -65,9 +65,24 @@ def workload(order: int):
     d = ts.Domain.aztec(order)
     t_max, _ = aztec_extremal_states(order)
     mask = d.vertex_mask
-    par = (np.add.outer(np.arange(d.n + 1), np.arange(d.n + 1)) & 1).astype(bool)
-    counts = (int((mask & ~par).sum()), int((mask & par).sum()))  # BLACK, WHITE
+    black, cols = 0, np.arange(d.n + 1)
+    for r0 in range(0, d.n + 1, 2048):  # row blocks: no n^2 integer temporaries
+        rows = np.arange(r0, min(d.n + 1, r0 + 2048))
+        black += int((mask[r0:r0 + 2048] & (((rows[:, None] + cols[None, :]) & 1) == 0)).sum())
+    counts = (black, int(mask.sum()) - black)  # BLACK, WHITE
     return d, t_max, counts
+
+
+MK = 2            # sweeps per domino_multi_kernel launch (kMK in csrc/domino.cu)
+GRAPH_SWEEPS = 32  # sweeps per CUDA-graph replay (kGraphSweeps)
+
+
+def launches_per_walk(n: int) -> int:
+    """Kernels one tsb_domino_walk of n sweeps launches: set_step, then per
+    graph replay a colour kernel, GRAPH_SWEEPS/MK multi-sweep kernels and the
+    step advance, then one single-sweep kernel per remaining sweep."""
+    replays = n // GRAPH_SWEEPS
+    return (1 + replays * (2 + GRAPH_SWEEPS // MK) if replays else 0) + n % GRAPH_SWEEPS
 
 
 def attempts_for(seed: int, step0: int, n: int, counts) -> int:
@@ -288,11 +303,14 @@ def main():
     max_ms = float(t.item())
     value = float(a.item()) / (max_ms / 1e3)
 
-    # roofline of the dominant kernel (domino_sweep_kernel: one launch per sweep)
+    # roofline of the dominant kernel: domino_multi_kernel, MK sweeps per
+    # launch, ~97% of the step (profiles/round1_launches_4096.txt); achieved =
+    # algorithmic bytes per launch / average launch interval on the stream
     n_domain = counts[0] + counts[1]
     n_rank = strip_vertices if strips else n_domain
-    per_launch_ms = total_ms / (args.steps * S)
-    achieved = n_rank / (per_launch_ms / 1e3) / 1e9  # 1 B/vertex/sweep algorithmic
+    walk_len = args.halo if strips else S
+    per_launch_ms = total_ms / (args.steps * S / MK)
+    achieved = MK * n_rank / (per_launch_ms / 1e3) / 1e9  # 1 B/vertex/sweep algorithmic
     peak, peak_src = peaks()
 
     e2e = None
@@ -359,15 +377,16 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps; state planes stay "
                              "L2-resident within a step by design"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic("domino_sweep_kernel"),
+                         "frac": achieved / peak, "traffic": traffic("domino_multi_kernel"),
                          "traffic_source": "profiles/traffic.json (ncu --set full capture)",
-                         "kernel": "domino_sweep_kernel",
-                         "bytes_per_launch": n_rank, "peak_source": peak_src,
+                         "kernel": "domino_multi_kernel", "sweeps_per_launch": MK,
+                         "launch_ms": per_launch_ms,
+                         "bytes_per_launch": MK * n_rank, "peak_source": peak_src,
                          "accounting": "1 B per in-domain vertex per sweep (4-bit state read + write)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * S,
+            "gpu_launches": args.steps * (S // walk_len) * launches_per_walk(walk_len),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

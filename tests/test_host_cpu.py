@@ -195,3 +195,17 @@ def test_lozenge_host_side():
         dn = np.zeros((4, 4), bool)
         up[0, 0] = up[3, 3] = True
         ts.TriDomain((4, 4), up, dn)
+
+
+def test_aztec_closed_form_matches_brick_runs():
+    """The row-by-row Aztec extremal states equal the generic brick tilings."""
+    import numpy as np
+
+    from paper_1804_07250_b200.lattice import Domain, aztec_extremal_states, brick_tiling_states
+
+    for order in (1, 2, 3, 8, 31, 64, 129):
+        d = Domain.aztec(order)
+        hb, vb = brick_tiling_states(d, True), brick_tiling_states(d, False)
+        t_max, t_min = aztec_extremal_states(order)
+        exp = (hb, vb) if order % 2 == 0 else (vb, hb)
+        assert np.array_equal(t_max, exp[0]) and np.array_equal(t_min, exp[1]), order

@@ -3,7 +3,7 @@
 (reported in DESIGN.md; bench.py is the contract line).  Device-resident
 states, CUDA-event timing on the handle's stream after warm-up.
 
-    python tools/bench_configs.py [--only c1,c2,c3,c5] [--quick]
+    python tools/bench_configs.py [--only c1,c2,c3,c4,c5,mixed] [--quick]
 """
 
 from __future__ import annotations
@@ -137,9 +137,76 @@ def c5(torch, stream, quick):
             "attempts_per_s": chain_sweeps * int(d.vertex_mask.sum()) / 2 / dt}
 
 
+def _domino_counts(d):
+    """(BLACK, WHITE) in-domain vertices, row blocks (no n^2 integer temporaries)."""
+    mask = d.vertex_mask
+    black = 0
+    cols = np.arange(d.n + 1)
+    for r0 in range(0, d.n + 1, 2048):
+        rows = np.arange(r0, min(d.n + 1, r0 + 2048))
+        even = ((rows[:, None] + cols[None, :]) & 1) == 0
+        black += int((mask[r0:r0 + 2048] & even).sum())
+    return black, int(mask.sum()) - black
+
+
+def c4(torch, stream, quick):
+    """Aztec order 16384 on one GPU (the per-GPU share of BASELINE config 4
+    at N=1): 536,969,217 domain vertices, 2 x 277 MB of planes, HBM-resident."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200 import rng
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    order = 4096 if quick else 16384
+    d = ts.Domain.aztec(order)
+    t_max, _ = aztec_extremal_states(order)
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.upload(t_max[None])
+    del t_max
+    steps = 1024
+    h.walk([0x5EED], 64)
+    dt = timed(torch, stream, lambda: h.walk([0x5EED], steps, step0=64))
+    counts = _domino_counts(d)
+    att = sum(counts[rng.color_at(0x5EED, s)] for s in range(64, 64 + steps))
+    nv = counts[0] + counts[1]
+    gbs = nv * steps / dt / 1e9
+    return {"config": f"C4 aztec {order} T_max on 1 GPU, {steps} sweeps", "us_per_sweep": dt / steps * 1e6,
+            "attempts_per_s": att / dt, "domain_vertices": nv, "algorithmic_GBps": gbs}
+
+
+def mixed(torch, stream, quick):
+    """The headline workload after a long warm-up (Aztec 4096 from T_max,
+    2^21 sweeps), so the timed sweeps see a mixed state with many rotateable
+    sites (RNG-heavy), next to the fraction of rotateable vertices."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200 import rng
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    order, warm = (1024, 1 << 20) if quick else (4096, 1 << 21)
+    d = ts.Domain.aztec(order)
+    t_max, _ = aztec_extremal_states(order)
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.upload(t_max[None])
+    tw = timed(torch, stream, lambda: h.walk([0x5EED], warm))
+    st = h.download()[0]
+    rot = float(((st == 3) | (st == 12))[d.vertex_mask].mean())
+    steps = 1024
+    dt = timed(torch, stream, lambda: h.walk([0x5EED], steps, step0=warm))
+    counts = _domino_counts(d)
+    att = sum(counts[rng.color_at(0x5EED, s)] for s in range(warm, warm + steps))
+    return {"config": f"aztec {order} after {warm} warm-up sweeps from T_max, {steps} timed sweeps",
+            "rotateable_fraction": rot, "warm_us_per_sweep": tw / warm * 1e6, "us_per_sweep": dt / steps * 1e6,
+            "attempts_per_s": att / dt}
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--only", default="c1,c2,c3,c5")
+    p.add_argument("--only", default="c1,c2,c3,c4,c5,mixed")
     p.add_argument("--quick", action="store_true")
     args = p.parse_args()
     import torch
