@@ -112,6 +112,13 @@ int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *
  * the domain has no tiling (the reference returns None). */
 int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, int ref_c);
 
+/* On-device observables (stats.py:187-245).  Adds the
+ * indicator "domino-orientation" (1 where a face is covered by a horizontal
+ * domino, stats.py:187-200) of chains [chain0, chain0+n) to the caller's
+ * device accumulator acc_dev ((side-1)^2 uint32 counts, face-major); faces
+ * outside the domain stay 0.  density_map = acc / (#states added). */
+int tsb_domino_orientation_add(tsb_domino *h, int chain0, int n, uint32_t *acc_dev);
+
 /* ------------------------------------------------------------------ CFTP */
 /* Progress callback: (round, steps = sum_{i<=round} 2^i, samples collapsed so
  * far, batch size, user) -- the reference's progress hook (cftp.py:130-136). */
@@ -160,6 +167,13 @@ int tsb_sv_sync(tsb_sv *h);
  * chain_max / chain_min; heights to hmax / hmin (nullable).
  * TSB_E_INFEASIBLE when the ring heights are incompatible. */
 int tsb_sv_extremal(tsb_sv *h, const int32_t *ring, int chain_max, int chain_min, int32_t *hmax, int32_t *hmin);
+/* Indicator observables of stats.py:213-228 added to a device uint32
+ * accumulator: observable 0 "h-edge" (n, n+1), 1 "v-edge" (n+1, n),
+ * 2 "c-vertex" (n, n). */
+int tsb_sv_observe_add(tsb_sv *h, int chain0, int n, int observable, uint32_t *acc_dev);
+/* Face heights summed into a device int64 accumulator ((n+1)^2): the mean
+ * height function = acc / (#states added). */
+int tsb_sv_height_sum_add(tsb_sv *h, int chain0, int n, long long *acc_dev);
 int tsb_sv_coalesced(tsb_sv *h, int chain0, int npairs, uint8_t *flags);
 int tsb_sv_replicate(tsb_sv *h, int src, int dst0, int step, int n);
 /* sv_cftp (sixvertex.py:565-622): as tsb_domino_cftp with height grids. */

@@ -140,3 +140,46 @@ def loz_walk(edges: np.ndarray, seeds, p_up: np.ndarray, n_steps: int, step0: in
     lib().orc_loz_walk(_ptr(out), out.shape[0], out.shape[2], out.shape[3], _ptr(seeds), _ptr(p),
                        step0, n_steps)
     return out.astype(bool)
+
+
+# ---------------------------------------------------------------- observables
+# numpy restatements of the reference's statistics (stats.py:187-288); pinned
+# against tests/golden/observables.npz (make_golden.py make_observables).
+
+def domino_orientation(states: np.ndarray, faces: np.ndarray) -> np.ndarray:
+    """stats.py:187-200 domino_orientation_grid: 1.0 where the face is covered
+    by a horizontal domino (its left or right edge is interior to a domino,
+    tilestate bit 2 "down" of the face's top-left / top-right corner), 0.0 for
+    a vertical one, NaN outside the domain."""
+    s = np.asarray(states)
+    horiz = ((s[:-1, :-1] & 2) | (s[:-1, 1:] & 2)) != 0
+    return np.where(faces, horiz.astype(float), np.nan)
+
+
+def aztec_y_intercept(orient: np.ndarray) -> float:
+    """stats.py:270-288 on an orientation grid: end of the top frozen
+    horizontal cluster on the central column, relative to the centre row."""
+    n = orient.shape[0]
+    mid = n // 2
+    col = orient[:, mid]
+    rows = np.nonzero(~np.isnan(col))[0]
+    boundary = rows[0]
+    for r in rows:
+        if col[r] == 1.0:
+            boundary = r + 1
+        else:
+            break
+    return float(boundary - mid)
+
+
+def sv_edges(heights: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """config_from_heights (sixvertex.py:270-277): (h_edges, v_edges)."""
+    h = np.asarray(heights).astype(np.int64)
+    return (h[:-1, :] - h[1:, :]) == 1, (h[:, 1:] - h[:, :-1]) == 1
+
+
+def sv_c_vertex(h_edges: np.ndarray, v_edges: np.ndarray) -> np.ndarray:
+    """c-vertex indicator (stats.py:225-228, vertex_type_codes sixvertex.py:236-239)."""
+    hh, vv = h_edges.astype(np.int8), v_edges.astype(np.int8)
+    codes = hh[:, :-1] + 2 * hh[:, 1:] + 4 * vv[:-1, :] + 8 * vv[1:, :]
+    return (codes == 0b1001) | (codes == 0b0110)

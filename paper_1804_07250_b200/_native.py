@@ -96,6 +96,9 @@ _SIGS = {
     "tsb_domino_heights": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_domino_extremal": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_coalesced": (_i, [_vp, _i, _i, _vp]),
+    "tsb_domino_orientation_add": (_i, [_vp, _i, _i, _vp]),
+    "tsb_sv_observe_add": (_i, [_vp, _i, _i, _i, _vp]),
+    "tsb_sv_height_sum_add": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_replicate": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_cftp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
     "tsb_sv_create": (_i, [_i, _i, _i, _vp]),

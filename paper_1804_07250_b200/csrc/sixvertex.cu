@@ -628,6 +628,70 @@ static int sv_ensure_graph(tsb_sv *h, int chain0, int n) {
     return TSB_OK;
 }
 
+// On-device observables (stats.py:213-245 density_map of "h-edge", "v-edge",
+// "c-vertex").  Edge occupancies from the 1-bit state: between faces X -> Y,
+// Y = X + 1 iff (bit X == bit Y) xor (X has odd parity);
+//   v_edges[r, c] = h(r, c+1) - h(r, c) == 1          (sixvertex.py:270-277)
+//   h_edges[r, c] = h(r, c) - h(r+1, c) == 1
+//   c-vertex (r, c): code W + 2E + 4N + 8S in {0b1001, 0b0110} with
+//   W = h_edges[r, c], E = h_edges[r, c+1], N = v_edges[r, c], S = v_edges[r+1, c]
+//   (vertex_type_codes, sixvertex.py:236-239; stats.py:225-228).
+__device__ __forceinline__ uint32_t sv_odd_mask(int r, int p0) {  // bit b: (r + b + p0) odd (32w is even)
+    return ((r + p0) & 1) ? 0x55555555u : 0xAAAAAAAAu;
+}
+__device__ __forceinline__ uint32_t sv_vedge(const uint32_t *row, int w, int r, int p0) {
+    const uint32_t b = row[w], bn = (b >> 1) | (row[w + 1] << 31);
+    return ~(b ^ bn) ^ sv_odd_mask(r, p0);
+}
+__device__ __forceinline__ uint32_t sv_hedge(const uint32_t *row, const uint32_t *below, int w, int r, int p0) {
+    return ~(row[w] ^ below[w]) ^ sv_odd_mask(r + 1, p0);
+}
+
+// obs 0: h-edge (n, n+1); 1: v-edge (n+1, n); 2: c-vertex (n, n).  One thread
+// per (row, 32-site word), chains summed in registers.
+__global__ void sv_observe_kernel(const uint32_t *bits, const int32_t *h00, size_t chain_words, int pitch, int nchains,
+                                  int n, int obs, uint32_t *acc) {
+    const int rows = obs == 1 ? n + 1 : n, cols = obs == 0 ? n + 1 : n;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (r >= rows || w * 32 >= cols) return;
+    uint32_t cnt[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) cnt[b] = 0;
+    for (int z = 0; z < nchains; ++z) {
+        const uint32_t *P = bits + (size_t)z * chain_words + pitch;  // face row 0
+        const uint32_t *row = P + (size_t)r * pitch;
+        const int p0 = h00[z] & 1;
+        uint32_t m;
+        if (obs == 0) {
+            m = sv_hedge(row, row + pitch, w, r, p0);
+        } else if (obs == 1) {
+            m = sv_vedge(row, w, r, p0);
+        } else {
+            const uint32_t hw = sv_hedge(row, row + pitch, w, r, p0);
+            const uint32_t he = (hw >> 1) | (sv_hedge(row, row + pitch, w + 1, r, p0) << 31);
+            const uint32_t vn = sv_vedge(row, w, r, p0), vs = sv_vedge(row + pitch, w, r + 1, p0);
+            m = (hw & ~he & ~vn & vs) | (~hw & he & vn & ~vs);
+        }
+#pragma unroll
+        for (int b = 0; b < 32; ++b) cnt[b] += (m >> b) & 1u;
+    }
+    uint32_t *a = acc + (size_t)r * cols + (size_t)w * 32;
+    const int lim = min(32, cols - w * 32);
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+        if (b < lim) a[b] += cnt[b];
+}
+
+// Sum of face heights over chains (mean height function), int64 per face.
+__global__ void sv_height_sum_kernel(const int32_t *h, int nchains, size_t nf, long long *acc) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    long long s = 0;
+    for (int z = 0; z < nchains; ++z) s += h[(size_t)z * nf + i];
+    acc[i] += s;
+}
+
 int sv_check(tsb_sv *h, int chain0, int n) {
     if (!h) return fail(TSB_E_VALUE, "null handle");
     if (chain0 < 0 || n < 0 || chain0 + n > h->nchains)
@@ -881,6 +945,34 @@ int tsb_sv_extremal(tsb_sv *h, const int32_t *ring, int chain_max, int chain_min
         if (dst) std::copy(g.begin(), g.end(), dst);
     }
     cudaFree(dg);
+    return TSB_OK;
+}
+
+int tsb_sv_observe_add(tsb_sv *h, int chain0, int n, int observable, uint32_t *acc_dev) {
+    int rc = sv_check(h, chain0, n);
+    if (rc || n == 0) return rc;
+    if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");
+    if (observable < 0 || observable > 2) return fail(TSB_E_VALUE, "observable must be 0 (h-edge), 1 (v-edge), 2 (c-vertex)");
+    TSB_CUDA(cudaSetDevice(h->device));
+    const int rows = observable == 1 ? h->n + 1 : h->n, cols = observable == 0 ? h->n + 1 : h->n;
+    const int W = (cols + 31) / 32;
+    sv_observe_kernel<<<dim3((W + 63) / 64, rows), 64, 0, h->stream>>>(h->bits + (size_t)chain0 * h->chain_words,
+                                                                       h->h00 + chain0, h->chain_words, h->pitch, n,
+                                                                       h->n, observable, acc_dev);
+    TSB_CUDA(cudaGetLastError());
+    return TSB_OK;
+}
+
+int tsb_sv_height_sum_add(tsb_sv *h, int chain0, int n, long long *acc_dev) {
+    int rc = sv_check(h, chain0, n);
+    if (rc || n == 0) return rc;
+    if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");
+    TSB_CUDA(cudaSetDevice(h->device));
+    if ((rc = sv_hbuf(h, n))) return rc;
+    if ((rc = sv_unpack_dev(h, chain0, n, h->hbuf))) return rc;
+    const size_t nf = (size_t)h->f * h->f;
+    sv_height_sum_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, h->stream>>>(h->hbuf, n, nf, acc_dev);
+    TSB_CUDA(cudaGetLastError());
     return TSB_OK;
 }
 

@@ -221,7 +221,41 @@ def make_lozenge():
     save("lozenge.npz", **arrays)
 
 
+# ------------------------------------------------------------- observables
+def make_observables():
+    """density_map / domino_orientation_grid / aztec_y_intercept /
+    c_vertex_count (stats.py:187-288) of reference-sampled states."""
+    from tilesampler import stats
+
+    arrays = {}
+    # dominoes: Aztec 32, 6 chains from T_max after 300 and 600 sweeps
+    d = ts.Domain.aztec(32)
+    t_max, _ = ts.extremal_tilings(d)
+    plan = ts.SweepPlan(d)
+    seeds = np.array([1, 2, 3, 4, 5, 6], dtype=np.uint64)
+    s1 = ts.random_walk_batch(np.stack([t_max.states] * 6), seeds, 300, plan)
+    s2 = ts.random_walk_batch(s1, seeds + np.uint64(100), 300, plan)
+    states = np.concatenate([s1, s2])
+    arc = stats.SampleArchive("domino", {}, [ts.Tiling(d, s) for s in states])
+    arrays["dom_states"] = states
+    arrays["dom_density"] = stats.density_map(arc, "domino-orientation").grid
+    arrays["dom_orient0"] = stats.domino_orientation_grid(ts.Tiling(d, states[0]))
+    arrays["dom_yint"] = np.array([stats.aztec_y_intercept(ts.Tiling(d, s)) for s in states])
+    # six-vertex: DWBC 24, 4 chains from h_min / h_max after 150 sweeps
+    n = 24
+    hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+    start = np.stack([lo.heights, hi.heights, lo.heights, hi.heights])
+    hs = sv_random_walk_batch(start, np.array([7, 8, 9, 10], dtype=np.uint64), 150, ts.SVWeights(1.0, 1.0, 1.5))
+    cfgs = [ts.config_from_heights(ts.FaceHeights(n, h)) for h in hs]
+    arc = stats.SampleArchive("sixvertex", {}, cfgs)
+    arrays["sv_heights"] = hs
+    for name in ("h-edge", "v-edge", "c-vertex"):
+        arrays["sv_" + name.replace("-", "_")] = stats.density_map(arc, name).grid
+    arrays["sv_ccount"] = np.array([stats.c_vertex_count(c) for c in cfgs])
+    save("observables.npz", **arrays)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge"]
+    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables"]
     for w in which:
         globals()[f"make_{w}"]()

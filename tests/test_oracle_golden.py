@@ -102,3 +102,21 @@ def test_lozenge_cases():
         assert np.array_equal(out, g[f"l{i}_out"]), f"loz case {i}"
         i += 1
     assert i == 3
+
+
+def test_oracle_observables_match_reference():
+    """The oracle's restated statistics equal the reference's stats.py outputs."""
+    import paper_1804_07250_b200 as ts
+
+    g = np.load(os.path.join(G, "observables.npz"))
+    d = ts.Domain.aztec(32)
+    grids = [oracle.domino_orientation(s, d.faces) for s in g["dom_states"]]
+    assert np.array_equal(grids[0], g["dom_orient0"], equal_nan=True)
+    assert np.allclose(np.mean(grids, axis=0), g["dom_density"], equal_nan=True, rtol=0, atol=1e-15)
+    assert [oracle.aztec_y_intercept(x) for x in grids] == list(g["dom_yint"])
+    he, ve, cv = zip(*[(*oracle.sv_edges(h), None) for h in g["sv_heights"]])
+    cv = [oracle.sv_c_vertex(a, b) for a, b in zip(he, ve)]
+    assert np.array_equal(np.mean(he, axis=0), g["sv_h_edge"])
+    assert np.array_equal(np.mean(ve, axis=0), g["sv_v_edge"])
+    assert np.array_equal(np.mean(cv, axis=0), g["sv_c_vertex"])
+    assert [int(c.sum()) for c in cv] == list(g["sv_ccount"])
