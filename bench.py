@@ -80,9 +80,14 @@ GRAPH_SWEEPS = 32  # sweeps per CUDA-graph replay (kGraphSweeps)
 def launches_per_walk(n: int) -> int:
     """Kernels one tsb_domino_walk of n sweeps launches: set_step, then per
     graph replay a colour kernel, GRAPH_SWEEPS/MK multi-sweep kernels and the
-    step advance, then one single-sweep kernel per remaining sweep."""
-    replays = n // GRAPH_SWEEPS
-    return (1 + replays * (2 + GRAPH_SWEEPS // MK) if replays else 0) + n % GRAPH_SWEEPS
+    step advance; the remainder as direct multi-sweep launches (plus a colour
+    kernel) and at most one single-sweep kernel."""
+    replays, rem = divmod(n, GRAPH_SWEEPS)
+    k = 1 + replays * (2 + GRAPH_SWEEPS // MK) if replays else 0
+    if rem >= MK:  # remainder: (set_step,) colour kernel, direct multi-sweep launches
+        k += (0 if replays else 1) + 1 + rem // MK
+        rem %= MK
+    return k + rem
 
 
 def attempts_for(seed: int, step0: int, n: int, counts) -> int:

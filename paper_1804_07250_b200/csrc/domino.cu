@@ -721,6 +721,13 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
         TSB_CUDA(cudaGetLastError());
         for (; s + kGraphSweeps <= n_steps; s += kGraphSweeps) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
     }
+    if (n_steps - s >= (uint64_t)kMK) {  // remainder: direct multi-sweep launches (step_dev = step0 + s)
+        if (s == 0) set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        colors_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
+        TSB_CUDA(cudaGetLastError());
+        for (uint64_t i = 0; s + kMK <= n_steps; s += kMK, i += kMK)
+            if ((rc = launch_multi(h, chain0, n, i, h->stream))) return rc;
+    }
     for (; s < n_steps; ++s)
         if ((rc = launch_sweep(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;
     return settle(h, chain0, n, cur0);

@@ -696,8 +696,10 @@ int lz_graph(tsb_loz *h, int chain0, int n) {
     return TSB_OK;
 }
 
-int lz_settle(tsb_loz *h, int chain0, int n, uint64_t nsweeps) {
-    if ((nsweeps & 1) == 0 || n == h->nchains) return TSB_OK;
+// After a walk the walked chains live in buf[cur]; when that is not the
+// buffer the other chains live in (cur0), copy them back.
+int lz_settle(tsb_loz *h, int chain0, int n, int cur0) {
+    if (h->cur == cur0 || n == h->nchains) return TSB_OK;
     const size_t off = (size_t)chain0 * h->chain_words;
     TSB_CUDA(cudaMemcpyAsync(h->buf[h->cur ^ 1] + off, h->buf[h->cur] + off, sizeof(uint32_t) * h->chain_words * n,
                              cudaMemcpyDeviceToDevice, h->stream));
@@ -943,6 +945,7 @@ int tsb_loz_walk(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t 
     if (!seeds) return fail(TSB_E_VALUE, "null seeds");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = lz_push_seeds(h, n, seeds))) return rc;
+    const int cur0 = h->cur;
     uint64_t s = 0;
     if (n_steps >= 2 * kLzGraph) {
         if ((rc = lz_graph(h, chain0, n))) return rc;
@@ -950,9 +953,15 @@ int tsb_loz_walk(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t 
         TSB_CUDA(cudaGetLastError());
         for (; s + kLzGraph <= n_steps; s += kLzGraph) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
     }
+    if (n_steps - s >= (uint64_t)h->m_K) {  // remainder: direct multi-sweep launches (step_dev = step0 + s)
+        if (s == 0) lz_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        TSB_CUDA(cudaGetLastError());
+        for (uint64_t i = 0; s + h->m_K <= n_steps; s += h->m_K, i += h->m_K)
+            if ((rc = lz_launch_multi(h, chain0, n, i, h->stream))) return rc;
+    }
     for (; s < n_steps; ++s)
         if ((rc = lz_launch(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;
-    return lz_settle(h, chain0, n, n_steps);
+    return lz_settle(h, chain0, n, cur0);
 }
 
 int tsb_loz_sweep(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int color) {
@@ -961,8 +970,9 @@ int tsb_loz_sweep(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t
     if (color < 0 || color > 2) return fail(TSB_E_VALUE, "colour class must be 0, 1 or 2");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = lz_push_seeds(h, n, seeds))) return rc;
+    const int cur0 = h->cur;
     if ((rc = lz_launch(h, chain0, n, step, color, h->stream, nullptr))) return rc;
-    return lz_settle(h, chain0, n, 1);
+    return lz_settle(h, chain0, n, cur0);
 }
 
 int tsb_loz_sync(tsb_loz *h) {

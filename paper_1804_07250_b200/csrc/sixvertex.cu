@@ -875,6 +875,19 @@ static int sv_walk_impl(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uin
         for (uint64_t r = 0; r < replays; ++r) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
         done = replays * kSvGraphSweeps;
     }
+    if (class_override < 0 && n_steps - done >= (uint64_t)h->m_K) {
+        // remainder: direct multi-sweep launches bits -> bits2 -> ..., step_dev = step0 + done
+        if (done == 0) sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        int launches = 0;
+        for (uint64_t i = 0; done + h->m_K <= n_steps; done += h->m_K, i += h->m_K, ++launches)
+            if ((rc = sv_launch_multi(h, chain0, n, i, (launches & 1) ? h->bits2 : h->bits,
+                                      (launches & 1) ? h->bits : h->bits2, h->stream)))
+                return rc;
+        if (launches & 1)
+            TSB_CUDA(cudaMemcpyAsync(h->bits + (size_t)chain0 * h->chain_words,
+                                     h->bits2 + (size_t)chain0 * h->chain_words,
+                                     sizeof(uint32_t) * h->chain_words * n, cudaMemcpyDeviceToDevice, h->stream));
+    }
     for (uint64_t s = done; s < n_steps; ++s) {
         c.step = step0 + s;
         sv_sweep_kernel<<<grid, 32 * warps, 0, h->stream>>>(c);
