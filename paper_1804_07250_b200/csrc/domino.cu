@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
 // test; loads, stores, addressing and the launch are paid once per kMK sweeps.
 // Used inside the graph replays (colours from the per-replay table).
 template <int TM>
-__global__ void __launch_bounds__(32 * kMRows, 2) domino_multi_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint2(*vs)[32] = reinterpret_cast<uint2(*)[32]>(dsm);
     uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(32 * kMRows, 2) domino_multi_kernel(SweepCtx c
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
     if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
     const uint64_t step0 = *c.step_dev + c.step;
+    const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         const uint64_t step = step0 + (uint64_t)s;
@@ -183,9 +184,11 @@ __global__ void __launch_bounds__(32 * kMRows, 2) domino_multi_kernel(SweepCtx c
             vua = u.x;
             vub = u.y;
         }
-        const uint32_t act = ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u;
-        uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
-        if (lane == 0) hl = 0u;
+        const uint32_t act = color ? ~act0 : act0;
+        // lane 0's word a and lane 31's word b are halo words: their
+        // neighbour bits from the shuffles wrap around but only feed bits
+        // that are never stored (stale-halo argument above)
+        const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vua & cur.x & ~(la | cur.y);
         const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act;
@@ -200,13 +203,15 @@ __global__ void __launch_bounds__(32 * kMRows, 2) domino_multi_kernel(SweepCtx c
         fs[k][lane] = f;
         __syncthreads();
         const uint2 fn = k + 1 < kMRows ? fs[k + 1][lane] : make_uint2(0u, 0u);  // F(r+1)
-        uint32_t frb = __shfl_down_sync(0xffffffffu, f.x, 1);
-        if (lane == 31) frb = 0u;
+        const uint32_t frb = __shfl_down_sync(0xffffffffu, f.x, 1);
         const uint32_t nva = cur.x ^ f.x ^ fn.x;
         const uint32_t nvb = cur.z ^ f.y ^ fn.y;
         const uint32_t nha = cur.y ^ f.x ^ (f.x >> 1) ^ (f.y << 31);
         const uint32_t nhb = cur.w ^ f.y ^ (f.y >> 1) ^ (frb << 31);
-        cur = in_grid ? make_uint4(nva, nha, nvb, nhb) : make_uint4(0u, 0u, 0u, 0u);
+        // rows outside the grid stay zero without masking: a vertex on the
+        // first or last grid row is never rotateable (its outer edges cannot
+        // be crossed), so no fire reaches them
+        cur = make_uint4(nva, nha, nvb, nhb);
     }
     if (k >= kMK && k < kMRows - kMK && in_grid) {  // warp-uniform
         uint2 *out = c.dst + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
