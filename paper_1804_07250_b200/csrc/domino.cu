@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     const int k = threadIdx.x >> 5;
     const int2 tile = c.tiles[blockIdx.x];
     const int r = tile.y * kMOut - kMK + k;
-    const int wa = tile.x * kTileWords - 2 + 2 * lane;
+    const int wa = tile.x + 2 * lane;  // band-aligned tile: tile.x = first loaded word (even)
     const int z = blockIdx.z;
     const bool in_grid = r >= 0 && r < c.side;
     const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
@@ -509,8 +509,11 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     h->W = (side + 31) / 32;
     // rows: kPad zero words, W words, zero padding up to the last tile's halo;
     // 256-byte aligned
+    // right padding: the single-sweep tiles (multiples of kTileWords) and the
+    // band-aligned multi-sweep tiles (any even start <= W - 2, 64 words) both
+    // load and store inside the row
     const int nchunks_ = (h->W + 1 + kTileWords - 1) / kTileWords;
-    h->pitch = (kPad + nchunks_ * kTileWords + 2 + 31) / 32 * 32;
+    h->pitch = (std::max(kPad + nchunks_ * kTileWords + 2, kPad + h->W + 64) + 31) / 32 * 32;
     h->chain_stride = (size_t)(side + 2) * h->pitch;
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaStreamCreate"); }
@@ -581,7 +584,22 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     };
     std::vector<int2> tiles, mtiles;
     make_tiles(kTileRows, tiles, h->band_start);
-    make_tiles(kMOut, mtiles, h->mband_start);
+    {
+        // multi-sweep tiles are aligned to each band's own word range: tile.x
+        // = first loaded word wa0 (even, for 16-byte loads), outputs words
+        // wa0+1 .. wa0+kTileWords; a band [wl, wh) starts at (wl-1) & ~1
+        const int nb = (side + kMOut - 1) / kMOut;
+        h->mband_start.assign(nb + 1, 0);
+        for (int y = 0; y < nb; ++y) {
+            h->mband_start[y] = (int)mtiles.size();
+            int lo = INT_MAX, hi = INT_MIN;
+            for (int r = y * kMOut; r < std::min(side, (y + 1) * kMOut); ++r)
+                if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
+            if (hi <= lo) continue;
+            for (int wa0 = (lo - 1) & ~1; wa0 + 1 < hi; wa0 += kTileWords) mtiles.push_back(make_int2(wa0, y));
+        }
+        h->mband_start[nb] = (int)mtiles.size();
+    }
     h->ntiles = (int)tiles.size();
     h->nmtiles = (int)mtiles.size();
     h->win_t0 = 0;
