@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(32 * kLzMRows, 2) lz_multi_kernel(LzMCtx c) {
     const int k = threadIdx.x >> 5;
     const int2 tile = c.tiles[blockIdx.x];
     const int x = tile.y * c.out_rows - c.K + k;
-    const int wa = tile.x * kLzWords - 2 + 2 * lane, wb = wa + 1;
+    const int wa = tile.x + 2 * lane, wb = wa + 1;  // band-aligned tile: tile.x = first loaded word (even)
     const int z = blockIdx.z;
     const uint64_t gkey = c.seedinfo[2 * z + 1];
     const bool in_grid = x >= 0 && x < c.X;
@@ -805,15 +805,15 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
         while (kLzMRows - 2 * K < 2) K /= 2;
         h->m_K = K;
         h->m_out = kLzMRows - 2 * K;
+        // tiles aligned to each band's own word range: tile.x = first loaded
+        // word wa0 (even; loads are predicated to the row), outputs wa0+1 .. wa0+kLzWords
         std::vector<int2> mt;
         for (int y = 0; y * h->m_out < h->X; ++y) {
             int lo = INT_MAX, hi = INT_MIN;
             for (int x = y * h->m_out; x < std::min(h->X, (y + 1) * h->m_out); ++x)
                 if (rg[x].y > rg[x].x) { lo = std::min(lo, rg[x].x); hi = std::max(hi, rg[x].y); }
-            for (int cx = 0; cx < nchunks; ++cx) {
-                const int w0 = cx * kLzWords - 1;
-                if (hi > w0 && lo < w0 + kLzWords) mt.push_back(make_int2(cx, y));
-            }
+            if (hi <= lo) continue;
+            for (int wa0 = (lo - 1) & ~1; wa0 + 1 < hi; wa0 += kLzWords) mt.push_back(make_int2(wa0, y));
         }
         h->nmtiles = (int)mt.size();
         if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mt.size()))) != cudaSuccess)
