@@ -344,26 +344,46 @@ def main():
                "api": "StripWalker over DominoHandle; state resident, strip rows read back to pinned host each step",
                "clock": "host wall clock, max over ranks"}
     if not args.no_e2e and not strips:
-        t0_tiling = ts.Tiling(d, t_max)
-        ts.random_walk(t0_tiling, seed, S, plan)  # warm the cached handle
-        torch.cuda.synchronize()
-        cur = t0_tiling
+        # End to end through the public handle API with the reference's state
+        # layout: every step uploads the (B, V, V) uint8 tilestates from pinned
+        # host memory, walks S sweeps and downloads the new tilestates into
+        # pinned host memory; the output of step k is the input of step k+1.
+        side = d.n + 1
+        he = DominoHandle(d, side, 1)
+        he.set_p_up(plan.p_up)
+        bufs = [torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        bufs[0].numpy()[0] = t_max
+        he.upload(bufs[0].numpy())
+        he.walk([seed], S)  # warm the graph
+        he.download(out=bufs[1].numpy())
+        he.sync()
         e2e_att = 0
         t0 = time.perf_counter()
         for k in range(args.steps):
             sk = rng.derive_seed(seed, k, 7)
-            cur = ts.random_walk(cur, sk, S, plan)  # H2D states, S sweeps, D2H states
+            src, dst = bufs[k & 1].numpy(), bufs[(k + 1) & 1].numpy()
+            he.upload(src)              # H2D: tilestates (V*V B)
+            he.walk([sk], S)            # H2D: the seed (8 B); S sweeps
+            he.download(out=dst)        # D2H: tilestates (V*V B), synchronous
             e2e_att += attempts_for(sk, 0, S, counts)
         dt = time.perf_counter() - t0
+        # the plain call a user makes with pageable numpy arrays, for reference
+        cur = ts.Tiling(d, bufs[0].numpy()[0].copy())
+        ts.random_walk(cur, seed, S, plan)
+        t1 = time.perf_counter()
+        cur = ts.random_walk(cur, rng.derive_seed(seed, 99, 7), S, plan)
+        dt_plain = time.perf_counter() - t1
+        att_plain = attempts_for(rng.derive_seed(seed, 99, 7), 0, S, counts)
         e2e_v = torch.tensor([dt], dtype=torch.float64, device="cuda")
         e2e_a = torch.tensor([float(e2e_att)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e2e_v, op=dist.ReduceOp.MAX)
             dist.all_reduce(e2e_a, op=dist.ReduceOp.SUM)
-        side = d.n + 1
         e2e = {"value": float(e2e_a.item()) / float(e2e_v.item()), "unit": UNIT,
                "h2d_bytes_per_step": side * side + 8, "d2h_bytes_per_step": side * side,
-               "api": "paper_1804_07250_b200.random_walk (pageable numpy in/out), host wall clock"}
+               "api": "DominoHandle.upload / walk / download (reference uint8 tilestates, pinned host buffers), "
+                      "host wall clock",
+               "random_walk_pageable": att_plain / dt_plain}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

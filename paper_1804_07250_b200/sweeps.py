@@ -214,9 +214,14 @@ class DominoHandle:
         s = np.ascontiguousarray(states, dtype=np.uint8)
         _native.check(_native.lib().tsb_domino_upload(self._h, chain0, s.shape[0], _native.ptr(s)))
 
-    def download(self, chain0: int = 0, n: int | None = None) -> np.ndarray:
+    def download(self, chain0: int = 0, n: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        """States of chains [chain0, chain0+n) as (n, V, V) uint8; `out` (e.g. a
+        pinned host buffer) is filled in place when given."""
         n = self.nchains - chain0 if n is None else n
-        out = np.empty((n, self.side, self.side), dtype=np.uint8)
+        if out is None:
+            out = np.empty((n, self.side, self.side), dtype=np.uint8)
+        elif out.shape != (n, self.side, self.side) or out.dtype != np.uint8 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous uint8 array of shape {(n, self.side, self.side)}")
         _native.check(_native.lib().tsb_domino_download(self._h, chain0, n, _native.ptr(out)))
         return out
 
@@ -275,15 +280,14 @@ def random_walk_batch(
 ) -> np.ndarray:
     """Evolve a (B, V, V) batch for n_steps coupled cluster sweeps on the
     device (sweeps.py:278-316).  Chain b's result depends on seeds[b] only."""
-    states = np.asarray(states)
+    states = np.ascontiguousarray(states, dtype=np.uint8)  # no copy for a C-contiguous uint8 batch
     v = states.shape[-1]
     seeds = np.asarray(seeds, dtype=np.uint64)
-    out = states.astype(np.uint8, copy=True)
-    if n_steps <= 0 or out.shape[0] == 0:
-        return out
-    h = _handle_for(plan.domain, out.shape[0]) if plan.domain.n + 1 == v else _handle_for(None, out.shape[0], v)
+    if n_steps <= 0 or states.shape[0] == 0:
+        return states.copy()  # a new array, like the reference (sweeps.py:299)
+    h = _handle_for(plan.domain, states.shape[0]) if plan.domain.n + 1 == v else _handle_for(None, states.shape[0], v)
     h.set_p_up(plan.p_up)
-    h.upload(out)
+    h.upload(states)
     h.walk(seeds, n_steps)
     return h.download()
 
