@@ -24,6 +24,7 @@ oracle/, all host threads) on the same workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -55,6 +56,8 @@ def parse():
     p.add_argument("--replicas", action="store_true",
                    help="N>1: independent chains per GPU (weak scaling) instead of strip sharding")
     p.add_argument("--halo", type=int, default=32, help="strip sharding: halo rows = sweeps between exchanges")
+    p.add_argument("--host-exchange", action="store_true",
+                   help="strip sharding: host-driven NCCL halo exchange instead of the device push/pull kernels")
     return p.parse_args()
 
 
@@ -263,11 +266,21 @@ def main():
     h.set_p_up(plan.p_up)
     h.upload(t_max[None])
     if strips:
-        from paper_1804_07250_b200.strips import DominoStripEngine, StripWalker, strip_bounds
+        from paper_1804_07250_b200.strips import (DeviceStripWalker, DominoStripEngine, StripWalker,
+                                                  strip_bounds)
 
         bounds = strip_bounds(d.vertex_mask, world, min_rows=args.halo)
-        walker = StripWalker(None, bounds, rank, world, args.halo)
-        walker.engine = DominoStripEngine(h, walker.window)
+        row_engine = None
+        if args.host_exchange:  # halo rows through torch.distributed (NCCL) from the host
+            walker = StripWalker(None, bounds, rank, world, args.halo)
+            walker.engine = row_engine = DominoStripEngine(h, walker.window)
+        else:  # push/pull kernels over peer memory (CUDA IPC), no host round trip
+            walker = DeviceStripWalker(h, bounds, rank, world, args.halo)
+            row_engine = DominoStripEngine.__new__(DominoStripEngine)  # row readback helper only
+            row_engine.h, row_engine.torch, row_engine._native = h, torch, _native
+            nb = ctypes.c_int64()
+            _native.check(_native.lib().tsb_domino_row_bytes(h._h, ctypes.byref(nb)))
+            row_engine.row_bytes, row_engine.device = nb.value, torch.device("cuda", local)
         strip_vertices = int(d.vertex_mask[walker.lo:walker.hi].sum())
 
         def run(n, step0):
@@ -320,10 +333,9 @@ def main():
 
     e2e = None
     if not args.no_e2e and strips:
-        import ctypes
 
         rows = walker.hi - walker.lo
-        host = torch.empty(rows * walker.engine.row_bytes, dtype=torch.uint8, pin_memory=True)
+        host = torch.empty(rows * row_engine.row_bytes, dtype=torch.uint8, pin_memory=True)
         seeds_h = torch.empty(1, dtype=torch.int64, pin_memory=True)
         seeds_d = torch.empty(1, dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
@@ -334,14 +346,15 @@ def main():
             seeds_d.copy_(seeds_h, non_blocking=True)  # the step's input (its seed index)
             run(S, step)
             step += S
-            host.copy_(walker.engine.get_rows(walker.lo, rows), non_blocking=True)  # the step's result
+            host.copy_(row_engine.get_rows(walker.lo, rows), non_blocking=True)  # the step's result
             torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e_att = attempts_for(seed, step - args.steps * S, args.steps * S, counts)
         e2e = {"value": e2e_att / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": 8,
                "d2h_bytes_per_step": int(host.numel()),
-               "api": "StripWalker over DominoHandle; state resident, strip rows read back to pinned host each step",
+               "api": ("StripWalker (host NCCL exchange)" if args.host_exchange else "DeviceStripWalker")
+                      + " over DominoHandle; state resident, strip rows read back to pinned host each step",
                "clock": "host wall clock, max over ranks"}
     if not args.no_e2e and not strips:
         # End to end through the public handle API with the reference's state
@@ -397,7 +410,8 @@ def main():
             "data": "synthetic: Aztec diamond from the closed-form T_max, uniform weights",
             "config": {"workload": f"aztec{args.order}_uniform_from_Tmax", "order": args.order,
                        "domain_vertices": n_domain, "sweeps_per_step": S, "seed": SEED,
-                       "parallelism": (f"strips x{world}, halo {args.halo} rows (NCCL p2p every {args.halo} sweeps)"
+                       "parallelism": (f"strips x{world}, halo {args.halo} rows exchanged every {args.halo} sweeps "
+                                       + ("(host NCCL p2p)" if args.host_exchange else "(device push/pull over peer memory)")
                                        if strips else (f"replicas x{world}" if world > 1 else "single chain")),
                        "l2": "flushed (256 MiB write) between timed steps; state planes stay "
                              "L2-resident within a step by design"},
@@ -415,6 +429,10 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank finished pushing into its neighbours' exchange regions
+        if strips and not args.host_exchange:
+            walker.close()
         dist.destroy_process_group()
 
 

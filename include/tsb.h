@@ -102,6 +102,31 @@ int tsb_domino_row_bytes(tsb_domino *h, int64_t *bytes);
 int tsb_domino_get_rows(tsb_domino *h, int chain, int r0, int nrows, void *dev_dst);
 int tsb_domino_set_rows(tsb_domino *h, int chain, int r0, int nrows, const void *dev_src);
 
+/* Device-driven strip exchange (replaces the host-driven
+ * halo swap of strips.py): rank owns rows [lo, hi) of chain 0 and sweeps them
+ * plus `halo` rows per side; tsb_domino_strip_init allocates the exchange
+ * region (halo staging + flags) and writes its CUDA IPC handle (64 bytes,
+ * cudaIpcMemHandle_t) to ipc_handle_out (nullable); connect opens the up /
+ * down neighbours' handles (NULL at the lattice edge) -- or, for handles in
+ * one process, connect_local links them directly.  strip_walk enqueues
+ * n_steps sweeps with a peer-memory halo push + flag wait every `halo`
+ * sweeps entirely in the handle's stream (no host synchronisation);
+ * the strip rows are bit-identical to a single-GPU walk. */
+int tsb_domino_strip_init(tsb_domino *h, int lo, int hi, int halo, void *ipc_handle_out);
+int tsb_domino_strip_connect(tsb_domino *h, const void *up_handle, const void *dn_handle);
+int tsb_domino_strip_connect_local(tsb_domino *h, tsb_domino *up, tsb_domino *dn);
+int tsb_domino_strip_walk(tsb_domino *h, uint64_t seed, uint64_t step0, uint64_t n_steps);
+/* The same walk one round at a time: strip_seed once, then per round phase 0
+ * (k <= halo sweeps from step0, then push; epoch += 1) and phase 1 (flag wait
+ * + pull).  Running phase 0 on all ranks before phase 1 lets several handles
+ * share one GPU (tests) without depending on concurrent streams. */
+int tsb_domino_strip_seed(tsb_domino *h, uint64_t seed);
+int tsb_domino_strip_step(tsb_domino *h, uint64_t step0, uint64_t k, int phase);
+/* Synchronise and report: TSB_E_CUDA if a flag wait gave up (~20 s without
+ * the neighbour's push; the epoch is returned in timed_out_epoch). */
+int tsb_domino_strip_status(tsb_domino *h, uint64_t *epoch, uint64_t *timed_out_epoch);
+int tsb_domino_strip_close(tsb_domino *h);
+
 /* Height function of chain `chain` (lattice.py:537-580): int32 (side x side),
  * 0 outside Domain.vertex_mask, h(ref) = 0 at the reference vertex
  * (lattice.py:197-203).  TSB_E_INCONSISTENT when the state does not

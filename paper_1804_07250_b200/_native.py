@@ -97,6 +97,14 @@ _SIGS = {
     "tsb_domino_extremal": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_orientation_add": (_i, [_vp, _i, _i, _vp]),
+    "tsb_domino_strip_init": (_i, [_vp, _i, _i, _i, _vp]),
+    "tsb_domino_strip_connect": (_i, [_vp, _vp, _vp]),
+    "tsb_domino_strip_connect_local": (_i, [_vp, _vp, _vp]),
+    "tsb_domino_strip_walk": (_i, [_vp, _u64, _u64, _u64]),
+    "tsb_domino_strip_seed": (_i, [_vp, _u64]),
+    "tsb_domino_strip_step": (_i, [_vp, _u64, _u64, _i]),
+    "tsb_domino_strip_status": (_i, [_vp, _vp, _vp]),
+    "tsb_domino_strip_close": (_i, [_vp]),
     "tsb_sv_observe_add": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_sv_height_sum_add": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_replicate": (_i, [_vp, _i, _i, _i, _i]),

@@ -627,6 +627,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
 int tsb_domino_destroy(tsb_domino *h) {
     if (!h) return TSB_OK;
     cudaSetDevice(h->device);
+    strip_free(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
     cudaFree(h->buf[0]);
     cudaFree(h->buf[1]);
@@ -736,6 +737,17 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
     if (!seeds) return fail(TSB_E_VALUE, "null seeds");
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = push_seeds(h, n, seeds))) return rc;
+    return walk_steps(h, chain0, n, step0, n_steps);
+}
+
+}  // extern "C"
+
+// n_steps sweeps of chains [chain0, chain0+n) whose seeds are already on the
+// device: graph replays, direct multi-sweep launches, single sweeps; the
+// walked chains end in the handle's canonical buffer.  Stream-ordered, no
+// host synchronisation.
+int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps) {
+    int rc;
     const int cur0 = h->cur;
     uint64_t s = 0;
     if (n_steps >= kGraphSweeps) {
@@ -755,6 +767,8 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
         if ((rc = launch_sweep(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;
     return settle(h, chain0, n, cur0);
 }
+
+extern "C" {
 
 int tsb_domino_sweep(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step, int color) {
     int rc = check_range(h, chain0, n);

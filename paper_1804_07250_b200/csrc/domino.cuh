@@ -40,6 +40,7 @@ struct tsb_domino {
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
     uint64_t g_t0 = 0, g_t1 = 0;
     int g_win0 = -1, g_winn = -1, g_winm = -1;
+    struct tsb_strip *strip = nullptr;  // device-driven strip exchange (strips.cu), if set up
 };
 
 constexpr int kGraphSweeps = 32;
@@ -53,4 +54,6 @@ int push_seeds(tsb_domino *h, int n, const uint64_t *seeds);
 int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_override, cudaStream_t stream,
                  const uint64_t *step_dev);
 int settle(tsb_domino *h, int chain0, int n, int cur0);
+int walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps);
+void strip_free(tsb_domino *h);
 }  // namespace tsb

@@ -135,3 +135,100 @@ class DominoStripEngine:
     def set_rows(self, r0: int, n: int, buf):
         self._native.check(self._native.lib().tsb_domino_set_rows(self.h._h, 0, r0, n,
                                                                   ctypes.c_void_p(buf.data_ptr())))
+
+
+class DeviceStripWalker:
+    """Strip walk with the halo exchange in device code (csrc/strips.cu).
+
+    Each rank's `DominoHandle` (chain 0 = the whole lattice) sweeps rows
+    [lo, hi) plus `halo` rows per side; every `halo` sweeps the boundary rows
+    are pushed into the neighbours' exchange regions over peer memory
+    (NVLink / NVSwitch; CUDA IPC between processes) and pulled after a flag
+    wait, all in the handle's stream.  `walk` only enqueues work: the host
+    never waits on a neighbour.  Bit-identical to the single-GPU walk.
+
+    Across processes the 64-byte IPC handles are exchanged once through
+    `torch.distributed` (any backend); `DeviceStripWalker.local(handles, ...)`
+    links handles of one process directly (tests on one GPU).
+    """
+
+    def __init__(self, handle, bounds: list[int], rank: int, world: int, halo: int, group=None,
+                 connect: bool = True):
+        from . import _native
+
+        self.handle = handle
+        self.rank, self.world = rank, world
+        self.lo, self.hi = bounds[rank], bounds[rank + 1]
+        self.halo = halo
+        if world > 1 and min(b1 - b0 for b0, b1 in zip(bounds, bounds[1:])) < halo:
+            raise ValueError("every strip needs at least `halo` rows")
+        self.window = (max(0, self.lo - halo), min(bounds[-1], self.hi + halo))
+        self._ipc = ctypes.create_string_buffer(64)
+        L = _native.lib()
+        _native.check(L.tsb_domino_strip_init(handle._h, self.lo, self.hi, halo, self._ipc))
+        if connect and world > 1:
+            import torch.distributed as dist
+
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(self._ipc.raw), group=group)
+            up = ctypes.create_string_buffer(handles[rank - 1], 64) if rank > 0 else None
+            dn = ctypes.create_string_buffer(handles[rank + 1], 64) if rank < world - 1 else None
+            _native.check(L.tsb_domino_strip_connect(handle._h, up, dn))
+            dist.barrier(group=group)  # every region is mapped before the first push
+
+    @staticmethod
+    def walk_lockstep(walkers: list["DeviceStripWalker"], seed: int, n_steps: int, step0: int = 0) -> None:
+        """Walk handles of ONE process round by round: every rank's sweeps and
+        push, then every rank's pull (the flag waits never spin), with a host
+        synchronisation between the halves.  For several strips on one GPU."""
+        from . import _native
+
+        L = _native.lib()
+        for w in walkers:
+            _native.check(L.tsb_domino_strip_seed(w.handle._h, _native.u64(seed)))
+        done = 0
+        while done < n_steps:
+            k = min(walkers[0].halo, n_steps - done)
+            for w in walkers:
+                _native.check(L.tsb_domino_strip_step(w.handle._h, _native.u64(step0 + done), _native.u64(k), 0))
+            for w in walkers:
+                w.handle.sync()
+            for w in walkers:
+                _native.check(L.tsb_domino_strip_step(w.handle._h, _native.u64(0), _native.u64(0), 1))
+            for w in walkers:
+                w.handle.sync()
+            done += k
+
+    @classmethod
+    def local(cls, handles, bounds: list[int], halo: int) -> list["DeviceStripWalker"]:
+        """One walker per handle of this process, linked without IPC."""
+        from . import _native
+
+        ws = [cls(h, bounds, r, len(handles), halo, connect=False) for r, h in enumerate(handles)]
+        L = _native.lib()
+        for r, w in enumerate(ws):
+            up = handles[r - 1]._h if r > 0 else None
+            dn = handles[r + 1]._h if r < len(handles) - 1 else None
+            _native.check(L.tsb_domino_strip_connect_local(w.handle._h, up, dn))
+        return ws
+
+    def walk(self, seed: int, n_steps: int, step0: int = 0) -> None:
+        from . import _native
+
+        _native.check(_native.lib().tsb_domino_strip_walk(self.handle._h, _native.u64(seed), _native.u64(step0),
+                                                          int(n_steps)))
+
+    def status(self) -> int:
+        """Wait for the enqueued work; raises if a neighbour flag wait timed out.
+        Returns the number of exchanges so far."""
+        from . import _native
+
+        e = ctypes.c_uint64()
+        _native.check(_native.lib().tsb_domino_strip_status(self.handle._h, ctypes.byref(e), None))
+        return e.value
+
+    def close(self) -> None:
+        """Release the exchange region (after every rank finished walking)."""
+        from . import _native
+
+        _native.check(_native.lib().tsb_domino_strip_close(self.handle._h))

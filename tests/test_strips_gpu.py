@@ -55,3 +55,78 @@ def test_strips_two_processes_one_gpu(tmp_path, world):
     ref = ts.random_walk_batch(t_max[None], [SEED], STEPS, ts.SweepPlan(d))[0]
     got = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("world,halo,steps", [(2, 32, 300), (3, 24, 250), (4, 16, 97)])
+def test_device_strips_local(world, halo, steps):
+    """Device-driven halo exchange (csrc/strips.cu: walk + peer push, flag wait
+    + pull) between handles of one process on one GPU, in host lockstep:
+    bit-identical to one walk."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.strips import DeviceStripWalker, strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    order = 300
+    d = ts.Domain.aztec(order)
+    plan = ts.SweepPlan(d)
+    t_max, _ = aztec_extremal_states(order)
+    hs = []
+    for _ in range(world):
+        h = DominoHandle(d, d.n + 1, 1, device=0)
+        h.set_p_up(plan.p_up)
+        h.upload(t_max[None])
+        hs.append(h)
+    bounds = strip_bounds(d.vertex_mask, world, min_rows=halo)
+    ws = DeviceStripWalker.local(hs, bounds, halo)
+    DeviceStripWalker.walk_lockstep(ws, SEED, steps, step0=5)
+    for w in ws:
+        assert w.status() == -(-steps // halo)
+    got = np.concatenate([w.handle.download()[0][w.lo:w.hi] for w in ws])
+    for w in ws:
+        w.close()
+    ref = oracle_walk(t_max, plan.p_up, steps, 5)
+    assert np.array_equal(got, ref)
+
+
+def oracle_walk(start, p_up, steps, step0):
+    import oracle
+
+    return oracle.domino_walk(start[None].copy(), [SEED], p_up, steps, step0=step0)[0]
+
+
+def _ipc_worker(rank, world, port, out_dir, halo, steps):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.strips import DeviceStripWalker, strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    d = ts.Domain.aztec(ORDER)
+    t_max, _ = aztec_extremal_states(ORDER)
+    h = DominoHandle(d, d.n + 1, 1, device=0)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.upload(t_max[None])
+    w = DeviceStripWalker(h, strip_bounds(d.vertex_mask, world, min_rows=halo), rank, world, halo)
+    w.walk(SEED, steps)
+    np.save(os.path.join(out_dir, f"dstrip{rank}.npy"), h.download()[0][w.lo:w.hi])
+    dist.barrier()
+    w.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_strips_ipc_processes(tmp_path, world):
+    """The same exchange across processes through CUDA IPC handles (here all
+    processes share cuda:0; on the 8-GPU box each has its own GPU)."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+
+    halo, steps = 32, 200
+    mp.spawn(_ipc_worker, args=(world, _free_port(), str(tmp_path), halo, steps), nprocs=world, join=True)
+    d = ts.Domain.aztec(ORDER)
+    t_max, _ = aztec_extremal_states(ORDER)
+    ref = oracle_walk(t_max, ts.SweepPlan(d).p_up, steps, 0)
+    got = np.concatenate([np.load(tmp_path / f"dstrip{r}.npy") for r in range(world)])
+    assert np.array_equal(got, ref)
