@@ -441,7 +441,8 @@ __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev
 int ensure_graph(tsb_domino *h, int chain0, int n) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
                       h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
-                      h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0;
+                      h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0 &&
+                      h->g_tail == h->graph_tail;
     if (same) return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -455,6 +456,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
+    if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) {
         if (g) cudaGraphDestroy(g);
@@ -476,6 +478,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_win0 = h->win_t0;
     h->g_winn = h->win_tn;
     h->g_winm = h->win_m0;
+    h->g_tail = h->graph_tail;
     return TSB_OK;
 }
 

@@ -41,6 +41,9 @@ struct tsb_domino {
     uint64_t g_t0 = 0, g_t1 = 0;
     int g_win0 = -1, g_winn = -1, g_winm = -1;
     struct tsb_strip *strip = nullptr;  // device-driven strip exchange (strips.cu), if set up
+    // work captured at the end of every graph replay (strip exchange), null: none
+    int (*graph_tail)(tsb_domino *, cudaStream_t) = nullptr;
+    int (*g_tail)(tsb_domino *, cudaStream_t) = nullptr;
 };
 
 constexpr int kGraphSweeps = 32;
@@ -56,4 +59,5 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
 int settle(tsb_domino *h, int chain0, int n, int cur0);
 int walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps);
 void strip_free(tsb_domino *h);
+int strip_exchange(tsb_domino *h, cudaStream_t stream);
 }  // namespace tsb

@@ -35,7 +35,8 @@ struct tsb_strip {
     uint2 *peer_up = nullptr, *peer_dn = nullptr;  // neighbours' regions
     bool up_ipc = false, dn_ipc = false;
     unsigned int *counter = nullptr;  // push-kernel completion counter (own)
-    uint64_t epoch = 0;
+    uint64_t *epoch_dev = nullptr;    // rounds completed (device; read by push / pull)
+    uint64_t epoch = 0;               // rounds enqueued (host)
 };
 
 namespace tsb {
@@ -53,7 +54,8 @@ __device__ __forceinline__ void copy_rows(uint2 *dst, const uint2 *src, size_t n
 
 // push epoch e: own boundary rows into the neighbours' staging slots
 __global__ void strip_push_kernel(const uint2 *rows_top, const uint2 *rows_bot, uint2 *peer_up, uint2 *peer_dn,
-                                  size_t slot, uint64_t e, unsigned int *counter) {
+                                  size_t slot, const uint64_t *epoch_dev, unsigned int *counter) {
+    const uint64_t e = *epoch_dev + 1;  // this round's epoch (advanced after the pull)
     const int par = (int)(e & 1);
     if (peer_up) copy_rows(peer_up + (2 + par) * slot, rows_top, slot);  // up's from_dn[par]
     if (peer_dn) copy_rows(peer_dn + par * slot, rows_bot, slot);        // down's from_up[par]
@@ -71,8 +73,9 @@ __global__ void strip_push_kernel(const uint2 *rows_top, const uint2 *rows_bot, 
 }
 
 // pull epoch e: wait for both neighbours' pushes, then staging -> halo rows
-__global__ void strip_pull_kernel(uint2 *halo_top, uint2 *halo_bot, uint2 *region, size_t slot, uint64_t e,
-                                  int has_up, int has_dn) {
+__global__ void strip_pull_kernel(uint2 *halo_top, uint2 *halo_bot, uint2 *region, size_t slot,
+                                  const uint64_t *epoch_dev, int has_up, int has_dn) {
+    const uint64_t e = *epoch_dev + 1;
     __shared__ int timed_out;
     if (threadIdx.x == 0) {
         uint64_t *fl = region_flags(region, slot);
@@ -109,6 +112,25 @@ __global__ void strip_pull_kernel(uint2 *halo_top, uint2 *halo_bot, uint2 *regio
     }
 }
 
+__global__ void strip_epoch_advance(uint64_t *epoch_dev) { *epoch_dev += 1; }
+
+// Enqueue push, pull and epoch advance of one round on `stream` (also used
+// while capturing the walk graph: the round then replays with the sweeps).
+int strip_exchange(tsb_domino *h, cudaStream_t stream) {
+    tsb_strip *s = h->strip;
+    if (!s || (!s->peer_up && !s->peer_dn)) return TSB_OK;
+    uint2 *rows = h->buf[h->cur] + h->pitch;  // chain 0, row 0 (after the guard row)
+    strip_push_kernel<<<kStripBlocks, 256, 0, stream>>>(rows + (size_t)s->lo * h->pitch,
+                                                        rows + (size_t)(s->hi - s->halo) * h->pitch, s->peer_up,
+                                                        s->peer_dn, s->slot, s->epoch_dev, s->counter);
+    strip_pull_kernel<<<kStripBlocks, 256, 0, stream>>>(rows + (size_t)(s->lo - s->halo) * h->pitch,
+                                                        rows + (size_t)s->hi * h->pitch, s->region, s->slot,
+                                                        s->epoch_dev, s->peer_up != nullptr, s->peer_dn != nullptr);
+    strip_epoch_advance<<<1, 1, 0, stream>>>(s->epoch_dev);
+    TSB_CUDA(cudaGetLastError());
+    return TSB_OK;
+}
+
 void strip_free(tsb_domino *h) {
     tsb_strip *s = h->strip;
     if (!s) return;
@@ -117,8 +139,10 @@ void strip_free(tsb_domino *h) {
     if (s->dn_ipc && s->peer_dn) cudaIpcCloseMemHandle(s->peer_dn);
     cudaFree(s->region);
     cudaFree(s->counter);
+    cudaFree(s->epoch_dev);
     delete s;
     h->strip = nullptr;
+    h->graph_tail = nullptr;
 }
 
 }  // namespace tsb
@@ -143,10 +167,13 @@ int tsb_domino_strip_init(tsb_domino *h, int lo, int hi, int halo, void *ipc_han
     if (e == cudaSuccess) e = cudaMemset(s->region, 0, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&s->counter, sizeof(unsigned int));
     if (e == cudaSuccess) e = cudaMemset(s->counter, 0, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMalloc(&s->epoch_dev, sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMemset(s->epoch_dev, 0, sizeof(uint64_t));
     if (e == cudaSuccess && ipc_handle_out) e = cudaIpcGetMemHandle((cudaIpcMemHandle_t *)ipc_handle_out, s->region);
     if (e != cudaSuccess) {
         cudaFree(s->region);
         cudaFree(s->counter);
+        cudaFree(s->epoch_dev);
         delete s;
         return cuda_fail(e, "strip init");
     }
@@ -191,21 +218,21 @@ int tsb_domino_strip_step(tsb_domino *h, uint64_t step0, uint64_t k, int phase) 
     if (!h || !h->strip) return fail(TSB_E_VALUE, "strip not initialised");
     tsb_strip *s = h->strip;
     TSB_CUDA(cudaSetDevice(h->device));
+    if (!s->peer_up && !s->peer_dn) return phase == 0 && k ? walk_steps(h, 0, 1, step0, k) : TSB_OK;
     uint2 *rows = h->buf[h->cur] + h->pitch;  // chain 0, row 0 (after the guard row)
     int rc;
     if (phase == 0) {
         if (k && (rc = walk_steps(h, 0, 1, step0, k))) return rc;
         rows = h->buf[h->cur] + h->pitch;
-        if (!s->peer_up && !s->peer_dn) return TSB_OK;
-        const uint64_t e = ++s->epoch;
+        ++s->epoch;
         strip_push_kernel<<<kStripBlocks, 256, 0, h->stream>>>(rows + (size_t)s->lo * h->pitch,
                                                               rows + (size_t)(s->hi - s->halo) * h->pitch,
-                                                              s->peer_up, s->peer_dn, s->slot, e, s->counter);
+                                                              s->peer_up, s->peer_dn, s->slot, s->epoch_dev, s->counter);
     } else {
-        if (!s->peer_up && !s->peer_dn) return TSB_OK;
         strip_pull_kernel<<<kStripBlocks, 256, 0, h->stream>>>(rows + (size_t)(s->lo - s->halo) * h->pitch,
                                                               rows + (size_t)s->hi * h->pitch, s->region, s->slot,
-                                                              s->epoch, s->peer_up != nullptr, s->peer_dn != nullptr);
+                                                              s->epoch_dev, s->peer_up != nullptr, s->peer_dn != nullptr);
+        strip_epoch_advance<<<1, 1, 0, h->stream>>>(s->epoch_dev);
     }
     TSB_CUDA(cudaGetLastError());
     return TSB_OK;
@@ -219,9 +246,21 @@ int tsb_domino_strip_seed(tsb_domino *h, uint64_t seed) {
 
 int tsb_domino_strip_walk(tsb_domino *h, uint64_t seed, uint64_t step0, uint64_t n_steps) {
     if (!h || !h->strip) return fail(TSB_E_VALUE, "strip not initialised");
+    tsb_strip *s = h->strip;
     int rc = tsb_domino_strip_seed(h, seed);
-    for (uint64_t done = 0; !rc && done < n_steps;) {
-        const uint64_t k = std::min<uint64_t>((uint64_t)h->strip->halo, n_steps - done);
+    uint64_t done = 0;
+    if (!rc && s->halo == kGraphSweeps && n_steps >= (uint64_t)kGraphSweeps && (s->peer_up || s->peer_dn)) {
+        // full rounds: the walk graph's replay carries the exchange as its tail
+        // (push, pull, epoch advance), so one graph launch per round
+        h->graph_tail = strip_exchange;
+        const uint64_t rounds = n_steps / kGraphSweeps;
+        rc = walk_steps(h, 0, 1, step0, rounds * kGraphSweeps);
+        h->graph_tail = nullptr;
+        s->epoch += rounds;
+        done = rounds * kGraphSweeps;
+    }
+    for (; !rc && done < n_steps;) {
+        const uint64_t k = std::min<uint64_t>((uint64_t)s->halo, n_steps - done);
         rc = tsb_domino_strip_step(h, step0 + done, k, 0);
         if (!rc) rc = tsb_domino_strip_step(h, 0, 0, 1);
         done += k;

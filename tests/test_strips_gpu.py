@@ -110,20 +110,23 @@ def _ipc_worker(rank, world, port, out_dir, halo, steps):
     h.upload(t_max[None])
     w = DeviceStripWalker(h, strip_bounds(d.vertex_mask, world, min_rows=halo), rank, world, halo)
     w.walk(SEED, steps)
+    assert w.status() == -(-steps // halo)
     np.save(os.path.join(out_dir, f"dstrip{rank}.npy"), h.download()[0][w.lo:w.hi])
     dist.barrier()
     w.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_device_strips_ipc_processes(tmp_path, world):
+@pytest.mark.parametrize("world,halo", [(2, 32), (3, 32), (2, 16)])
+def test_device_strips_ipc_processes(tmp_path, world, halo):
     """The same exchange across processes through CUDA IPC handles (here all
-    processes share cuda:0; on the 8-GPU box each has its own GPU)."""
+    processes share cuda:0; on the 8-GPU box each has its own GPU).  halo 32
+    runs the rounds as graph replays with the exchange captured as their
+    tail, halo 16 as explicit per-round launches."""
     import paper_1804_07250_b200 as ts
     from paper_1804_07250_b200.lattice import aztec_extremal_states
 
-    halo, steps = 32, 200
+    steps = 200
     mp.spawn(_ipc_worker, args=(world, _free_port(), str(tmp_path), halo, steps), nprocs=world, join=True)
     d = ts.Domain.aztec(ORDER)
     t_max, _ = aztec_extremal_states(ORDER)
