@@ -11,11 +11,16 @@ One "step" = `--sweeps-per-step` consecutive sweeps (default 1000) of one
 chain; between timed steps L2 is flushed by writing a 256 MiB buffer
 (outside the events), each step timed with CUDA events on the launching
 stream, and the per-rank total is reduced with MAX over ranks.  With N > 1
-(torchrun) the one chain is strip-sharded over the GPUs (strong scaling):
-each rank sweeps its rows plus --halo halo rows and swaps halos with its
-neighbours over NCCL every --halo sweeps (paper_1804_07250_b200/strips.py);
---replicas runs independent chains instead (weak scaling).  Rank 0 prints
-one JSON line.
+(torchrun), --mode replicas runs one independent chain of the workload per
+GPU (weak scaling; the way an MCMC sampler uses more GPUs when one lattice
+fits a GPU) and --mode strips shards ONE chain into row strips (strong
+scaling): each rank sweeps its rows plus --halo halo rows and refreshes the
+halos from its neighbours every --halo sweeps with push/pull kernels over
+peer memory (csrc/strips.cu; --host-exchange: NCCL from the host instead).
+The default (auto) shards lattices above order 8192 (BASELINE config 4) and
+replicates smaller ones: at order 4096 a 1/8 strip is latency-bound
+(~4.4 us per sweep for the busiest strip vs 6.2 us for the whole lattice,
+profiles/round1_strips_compute.jsonl).  Rank 0 prints one JSON line.
 
 `--impl reference` times the reference algorithm's CPU path (the C port in
 oracle/, all host threads) on the same workload, rank 0 only.
@@ -53,8 +58,10 @@ def parse():
     p.add_argument("--sweeps-per-step", type=int, default=1000)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--replicas", action="store_true",
-                   help="N>1: independent chains per GPU (weak scaling) instead of strip sharding")
+    p.add_argument("--mode", default="auto", choices=["auto", "replicas", "strips"],
+                   help="N>1: independent chains per GPU (weak scaling) or one strip-sharded chain "
+                        "(strong scaling); auto = strips above order 8192")
+    p.add_argument("--replicas", action="store_true", help="alias for --mode replicas")
     p.add_argument("--halo", type=int, default=32, help="strip sharding: halo rows = sweeps between exchanges")
     p.add_argument("--host-exchange", action="store_true",
                    help="strip sharding: host-driven NCCL halo exchange instead of the device push/pull kernels")
@@ -223,7 +230,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak",
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": {"workload": f"aztec{args.order}_uniform_from_Tmax",
                                         "sweeps_per_step": per_step},
@@ -258,7 +265,10 @@ def main():
     S = args.sweeps_per_step
     stream = torch.cuda.current_stream()
 
-    strips = world > 1 and not args.replicas
+    mode = "replicas" if args.replicas else args.mode
+    if mode == "auto":
+        mode = "strips" if args.order > 8192 else "replicas"
+    strips = world > 1 and mode == "strips"
     if strips:
         seed = SEED  # one chain sharded over all GPUs
     h = DominoHandle(d, d.n + 1, 1)

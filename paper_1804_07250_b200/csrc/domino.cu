@@ -150,8 +150,24 @@ __global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
 // the only ones stored.  Per sweep it costs two block barriers and the fire
 // test; loads, stores, addressing and the launch are paid once per kMK sweeps.
 // Used inside the graph replays (colours from the per-replay table).
+#ifdef TSB_TIMING
+// Debug builds only (nvcc -DTSB_TIMING): %globaltimer stamps of block 0..N of
+// each multi-sweep launch in a replay -> g_tt[launch][block][phase].
+__device__ unsigned long long g_tt[16][2048][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TT(ph) \
+    if (threadIdx.x == 0 && blockIdx.x < 2048 && c.step / kMK < 16) g_tt[c.step / kMK][blockIdx.x][ph] = gtimer()
+#else
+#define TT(ph)
+#endif
+
 template <int TM>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
+    TT(0);
     extern __shared__ __align__(16) unsigned char dsm[];
     uint2(*vs)[32] = reinterpret_cast<uint2(*)[32]>(dsm);
     uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
@@ -167,7 +183,9 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     const bool in_grid = r >= 0 && r < c.side;
     const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    TT(1);
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    TT(2);
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
     if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
     const uint64_t step0 = *c.step_dev + c.step;
@@ -212,6 +230,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
         // first or last grid row is never rotateable (its outer edges cannot
         // be crossed), so no fire reaches them
         cur = make_uint4(nva, nha, nvb, nhb);
+        TT(3 + s);
     }
     if (k >= kMK && k < kMRows - kMK && in_grid) {  // warp-uniform
         uint2 *out = c.dst + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
@@ -219,6 +238,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
         else if (lane == 0) out[wa + 1] = make_uint2(cur.z, cur.w);
         else out[wa] = make_uint2(cur.x, cur.y);
     }
+    TT(5);
 }
 
 // Colours of the next kGraphSweeps sweeps of every chain (graph mode).
@@ -828,6 +848,14 @@ int tsb_domino_get_rows(tsb_domino *h, int chain, int r0, int nrows, void *dev_d
 int tsb_domino_set_rows(tsb_domino *h, int chain, int r0, int nrows, const void *dev_src) {
     return row_copy(h, chain, r0, nrows, const_cast<void *>(dev_src), false);
 }
+
+#ifdef TSB_TIMING
+int tsb_debug_timing(unsigned long long *out) {
+    TSB_CUDA(cudaDeviceSynchronize());
+    TSB_CUDA(cudaMemcpyFromSymbol(out, g_tt, sizeof(g_tt)));
+    return TSB_OK;
+}
+#endif
 
 int tsb_domino_sync(tsb_domino *h) {
     if (!h) return fail(TSB_E_VALUE, "null handle");

@@ -204,6 +204,44 @@ def mixed(torch, stream, quick):
             "attempts_per_s": att / dt}
 
 
+def strips(torch, stream, quick):
+    """Per-rank compute of strip-sharded Aztec walks (the strong-scaling
+    share of one GPU): for N = 2, 4, 8 the busiest rank's window (its strip +
+    32 halo rows per side) is swept alone on this GPU with the exchange
+    kernels disabled -- the pool has one GPU, so NVLink time is not included."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200 import _native
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.strips import strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    out = []
+    for order in ((1024,) if quick else (4096, 16384)):
+        d = ts.Domain.aztec(order)
+        t_max, _ = aztec_extremal_states(order)
+        h = DominoHandle(d, d.n + 1, 1)
+        h.set_stream(stream.cuda_stream)
+        h.set_p_up(ts.SweepPlan(d).p_up)
+        h.upload(t_max[None])
+        del t_max
+        steps = 1024 if order <= 4096 else 256
+        base = None
+        for world in (1, 2, 4, 8):
+            b = strip_bounds(d.vertex_mask, world, min_rows=32)
+            times = []
+            for r in range(world):
+                lo, hi = max(0, b[r] - 32), min(d.n + 1, b[r + 1] + 32)
+                _native.check(_native.lib().tsb_domino_set_window(h._h, lo, hi))
+                h.walk([0x5EED], 64)
+                times.append(timed(torch, stream, lambda: h.walk([0x5EED], steps, step0=64)) / steps)
+            _native.check(_native.lib().tsb_domino_set_window(h._h, 0, -1))
+            t = max(times)
+            base = base or t
+            out.append({"config": f"strips aztec {order}: busiest of {world} rank windows (halo 32), compute only",
+                        "us_per_sweep": t * 1e6, "compute_speedup": base / t})
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="c1,c2,c3,c4,c5,mixed")
