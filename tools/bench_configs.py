@@ -204,6 +204,37 @@ def mixed(torch, stream, quick):
             "attempts_per_s": att / dt}
 
 
+def c5full(torch, stream, quick):
+    """C5 to completion: exact CFTP samples of the Aztec diamond of order 512
+    (cftp_sample_many, coupled T_max / T_min chains, doubling rounds) for a
+    small batch; reports the round each sample coalesced in and the time."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.cftp import chain_master_seed
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+    from paper_1804_07250_b200 import _native
+
+    order, count = (64, 4) if quick else (512, 8)
+    d = ts.Domain.aztec(order)
+    t_max, t_min = aztec_extremal_states(order)
+    h = DominoHandle(d, d.n + 1, 2 * count + 2)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(ts.SweepPlan(d).p_up)
+    masters = np.array([chain_master_seed(0x5EED, k) for k in range(count)], dtype=np.uint64)
+    out = np.zeros((count, d.n + 1, d.n + 1), dtype=np.uint8)
+    rr = np.zeros(count, dtype=np.int32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc = _native.lib().tsb_domino_cftp(h._h, _native.ptr(t_max), _native.ptr(t_min), _native.ptr(masters), count,
+                                       40, _native.ptr(out), _native.ptr(rr), None, None)
+    dt = time.perf_counter() - t0
+    _native.check(rc)
+    sweeps = [2 * (2 ** (int(r) + 1) - 2) for r in rr]  # coupled chain-sweeps per sample (cftp.py:115-119)
+    return {"config": f"C5 CFTP aztec {order}, {count} exact samples to coalescence", "seconds": dt,
+            "collapsed_rounds": rr.tolist(), "chain_sweeps_per_sample": sweeps,
+            "seconds_per_sample": dt / count}
+
+
 def strips(torch, stream, quick):
     """Per-rank compute of strip-sharded Aztec walks (the strong-scaling
     share of one GPU): for N = 2, 4, 8 the busiest rank's window (its strip +
