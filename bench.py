@@ -273,7 +273,7 @@ def main():
         seed = SEED  # one chain sharded over all GPUs
     h = DominoHandle(d, d.n + 1, 1)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(plan.p_up)
+    h.set_plan(plan)
     h.upload(t_max[None])
     if strips:
         from paper_1804_07250_b200.strips import (DeviceStripWalker, DominoStripEngine, StripWalker,
@@ -373,7 +373,7 @@ def main():
         # pinned host memory; the output of step k is the input of step k+1.
         side = d.n + 1
         he = DominoHandle(d, side, 1)
-        he.set_p_up(plan.p_up)
+        he.set_plan(plan)
         bufs = [torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         bufs[0].numpy()[0] = t_max
         he.upload(bufs[0].numpy())

@@ -70,6 +70,10 @@ int tsb_domino_set_stream(tsb_domino *h, void *stream);
 /* SweepPlan.p_up, (side x side) float64 (sweeps.py:170-179).  Converted
  * exactly to integer thresholds: u < p  <=>  (x >> 11) < ceil(p * 2^53). */
 int tsb_domino_set_p_up(tsb_domino *h, const double *p_up);
+/* The same for p_up that depends only on the vertex parity (Uniform:
+ * 0.5 / 0.5; VolumeWeights without overrides: q^(+-4)/(1+q^(+-4)),
+ * sweeps.py:134-150): no (side x side) grid is built or stored. */
+int tsb_domino_set_p_up_parity(tsb_domino *h, double p_even, double p_odd);
 
 /* Tiling.states batch (n, side, side) uint8 <-> device state.  Upload
  * rejects grids that are not edge-consistent or that cross a non-crossable

@@ -83,6 +83,7 @@ _SIGS = {
     "tsb_domino_destroy": (_i, [_vp]),
     "tsb_domino_set_stream": (_i, [_vp, _vp]),
     "tsb_domino_set_p_up": (_i, [_vp, _vp]),
+    "tsb_domino_set_p_up_parity": (_i, [_vp, ctypes.c_double, ctypes.c_double]),
     "tsb_domino_upload": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_download": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),

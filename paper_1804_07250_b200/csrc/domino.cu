@@ -688,33 +688,32 @@ int tsb_domino_set_p_up(tsb_domino *h, const double *p_up) {
     if (!h || !p_up) return fail(TSB_E_VALUE, "null argument");
     TSB_CUDA(cudaSetDevice(h->device));
     const int64_t s = h->side;
+    // pass 1: uniform or parity-only thresholds need no grid on the device
+    uint64_t par[2] = {threshold_of(p_up[0]), s > 1 ? threshold_of(p_up[1]) : threshold_of(p_up[0])};
+    bool parity_ok = true;
+    for (int64_t r = 0; r < s && parity_ok; ++r)
+        for (int64_t c = 0; c < s; ++c)
+            if (threshold_of(p_up[r * s + c]) != par[(r + c) & 1]) {
+                parity_ok = false;
+                break;
+            }
+    if (parity_ok) return tsb_domino_set_p_up_parity(h, p_up[0], s > 1 ? p_up[1] : p_up[0]);
+    // pass 2: per-site thresholds
     std::vector<uint64_t> t((size_t)(s * s));
-    bool uniform = true;
-    uint64_t par[2] = {0, 0};
-    bool have[2] = {false, false}, parity_ok = true;
-    for (int64_t r = 0; r < s; ++r)
-        for (int64_t c = 0; c < s; ++c) {
-            const uint64_t v = threshold_of(p_up[r * s + c]);
-            t[(size_t)(r * s + c)] = v;
-            if (v != t[0]) uniform = false;
-            const int p = (int)((r + c) & 1);
-            if (!have[p]) { have[p] = true; par[p] = v; }
-            else if (par[p] != v) parity_ok = false;
-        }
-    if (uniform) {
-        h->tmode = 0;
-        h->t0 = h->t1 = t[0];
-    } else if (parity_ok) {
-        h->tmode = 1;
-        h->t0 = par[0];
-        h->t1 = par[1];
-    } else {
-        h->tmode = 2;
-        if (!h->tgrid) TSB_CUDA(cudaMalloc(&h->tgrid, sizeof(uint64_t) * t.size()));
-        TSB_CUDA(cudaMemcpyAsync(h->tgrid, t.data(), sizeof(uint64_t) * t.size(), cudaMemcpyHostToDevice,
-                                 h->stream));
-        TSB_CUDA(cudaStreamSynchronize(h->stream));
-    }
+    for (int64_t i = 0; i < s * s; ++i) t[(size_t)i] = threshold_of(p_up[i]);
+    h->tmode = 2;
+    if (!h->tgrid) TSB_CUDA(cudaMalloc(&h->tgrid, sizeof(uint64_t) * t.size()));
+    TSB_CUDA(cudaMemcpyAsync(h->tgrid, t.data(), sizeof(uint64_t) * t.size(), cudaMemcpyHostToDevice, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    return TSB_OK;
+}
+
+int tsb_domino_set_p_up_parity(tsb_domino *h, double p_even, double p_odd) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    const uint64_t t0 = threshold_of(p_even), t1 = threshold_of(p_odd);
+    h->tmode = t0 == t1 ? 0 : 1;
+    h->t0 = t0;
+    h->t1 = t1;
     return TSB_OK;
 }
 

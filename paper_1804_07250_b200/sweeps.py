@@ -169,6 +169,22 @@ class SweepPlan:
     def p_up(self) -> np.ndarray:
         return _p_up_grid(self.domain.n + 1, self.weights)
 
+    @cached_property
+    def p_up_parity(self) -> tuple[float, float] | None:
+        """(p_up at even, at odd vertices) when p_up depends only on the
+        parity (Uniform; VolumeWeights without overrides), else None -- the
+        same float64 values as p_up (_p_up_grid), without the V x V grid."""
+        w = self.weights
+        if isinstance(w, Uniform):
+            return 0.5, 0.5
+        if isinstance(w, VolumeWeights) and not w.overrides:
+            out = []
+            for p in (0, 1):
+                ratio = w.default ** (4 if p == 0 else -4)
+                out.append(ratio / (1.0 + ratio))
+            return out[0], out[1]
+        return None
+
 
 # -- device handles ------------------------------------------------------------
 
@@ -209,6 +225,18 @@ class DominoHandle:
             raise ValueError(f"p_up must be {(self.side, self.side)}")
         _native.check(_native.lib().tsb_domino_set_p_up(self._h, _native.ptr(p)))
         self._p_up_ref = p_up
+
+    def set_plan(self, plan: "SweepPlan"):
+        """Thresholds of a SweepPlan; parity-only p_up (the common case)
+        never materialises the V x V grid (8.6 GB at Aztec 16384)."""
+        if self._p_up_ref is plan:
+            return
+        par = plan.p_up_parity
+        if par is None:
+            self.set_p_up(plan.p_up)
+        else:
+            _native.check(_native.lib().tsb_domino_set_p_up_parity(self._h, float(par[0]), float(par[1])))
+        self._p_up_ref = plan
 
     def upload(self, states: np.ndarray, chain0: int = 0):
         s = np.ascontiguousarray(states, dtype=np.uint8)
@@ -286,7 +314,7 @@ def random_walk_batch(
     if n_steps <= 0 or states.shape[0] == 0:
         return states.copy()  # a new array, like the reference (sweeps.py:299)
     h = _handle_for(plan.domain, states.shape[0]) if plan.domain.n + 1 == v else _handle_for(None, states.shape[0], v)
-    h.set_p_up(plan.p_up)
+    h.set_plan(plan)
     h.upload(states)
     h.walk(seeds, n_steps)
     return h.download()
@@ -303,7 +331,7 @@ def sweep(
 ):
     """One sweep of `color` at `step` with family f's coins (sweeps.py:322-342)."""
     h = _handle_for(plan.domain, 1)
-    h.set_p_up(plan.p_up)
+    h.set_plan(plan)
     h.upload(t.states[None])
     h.sweep([f.seed], step, int(color))
     new = h.download()[0]
@@ -337,7 +365,7 @@ class DominoCftp:
         self.top0 = np.ascontiguousarray(top0, dtype=np.uint8)
         self.bot0 = np.ascontiguousarray(bot0, dtype=np.uint8)
         self.handle = _handle_for(domain, 2 * count + 2)
-        self.handle.set_p_up(plan.p_up)
+        self.handle.set_plan(plan)
 
     def run(self, masters, max_doublings: int, progress=None, trace=None) -> np.ndarray:
         masters = np.ascontiguousarray(masters, dtype=np.uint64)

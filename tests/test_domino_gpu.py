@@ -258,3 +258,36 @@ def test_strip_windows_on_one_device():
     full = ts.random_walk_batch(t_max[None], [0x5EED], steps, plan)[0]
     got = np.concatenate([walkers[r].engine.h.download()[0][bounds[r]:bounds[r + 1]] for r in range(2)])
     assert np.array_equal(got, full)
+
+
+def test_c4_size_walk_windows_vs_oracle():
+    """BASELINE config 4's lattice (Aztec order 16384, 1.07e9 vertices) on one
+    GPU: after 40 sweeps the whole state is edge-consistent and three row
+    bands (top, middle, bottom) equal the oracle's walk of those bands plus a
+    40-row margin (one sweep moves information by one row)."""
+    import oracle
+    from paper_1804_07250_b200.lattice import BIT_DOWN, BIT_LEFT, BIT_RIGHT, BIT_UP, aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    order, steps = 16384, 40
+    d = ts.Domain.aztec(order)
+    plan = ts.SweepPlan(d)
+    side = d.n + 1
+    t_max, _ = aztec_extremal_states(order)
+    h = DominoHandle(d, side, 1)
+    h.set_plan(plan)
+    h.upload(t_max[None])
+    h.walk([0x5EED], steps)
+    out = h.download()[0]
+    del h
+    for r0 in range(0, side, 2048):  # every crossed edge is seen from both of its vertices
+        blk = out[r0:r0 + 2049]
+        assert np.array_equal((blk[:-1] & BIT_DOWN) != 0, (blk[1:] & BIT_UP) != 0)
+        assert np.array_equal((blk[:, :-1] & BIT_RIGHT) != 0, (blk[:, 1:] & BIT_LEFT) != 0)
+    assert not np.array_equal(out, t_max)
+    mid = side // 2
+    for a, b in ((0, 64), (mid - 32, mid + 32), (side - 64, side)):
+        lo, hi = max(0, a - steps), min(side, b + steps)
+        rows = np.ascontiguousarray(t_max[lo:hi])
+        oracle.domino_walk_window(rows, lo, 0x5EED, np.full((hi - lo, side), 0.5), steps)
+        assert np.array_equal(rows[a - lo:b - lo], out[a:b]), (a, b)

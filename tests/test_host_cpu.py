@@ -209,3 +209,19 @@ def test_aztec_closed_form_matches_brick_runs():
         t_max, t_min = aztec_extremal_states(order)
         exp = (hb, vb) if order % 2 == 0 else (vb, hb)
         assert np.array_equal(t_max, exp[0]) and np.array_equal(t_min, exp[1]), order
+
+
+def test_p_up_parity_matches_grid():
+    """SweepPlan.p_up_parity gives the same float64 values as the p_up grid."""
+    import numpy as np
+
+    import paper_1804_07250_b200 as ts
+
+    d = ts.Domain.aztec(6)
+    for w in (ts.Uniform(), ts.VolumeWeights(0.7), ts.VolumeWeights(1.3)):
+        plan = ts.SweepPlan(d, w)
+        pe, po = plan.p_up_parity
+        par = np.add.outer(np.arange(d.n + 1), np.arange(d.n + 1)) & 1
+        assert (plan.p_up[par == 0] == pe).all() and (plan.p_up[par == 1] == po).all()
+    assert ts.SweepPlan(d, ts.VolumeWeights(0.7, {(2, 3): 0.4})).p_up_parity is None
+    assert ts.SweepPlan(d, ts.EdgeWeights(1.0, {((0, 0), (0, 1)): 2.0})).p_up_parity is None

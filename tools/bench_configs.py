@@ -43,7 +43,7 @@ def c1(torch, stream, quick):
     t_max, _ = aztec_extremal_states(64)
     h = DominoHandle(d, d.n + 1, 1)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.set_plan(ts.SweepPlan(d))
     h.upload(t_max[None])
     h.walk([0x5EED], 1000)
     fp = hashlib.sha256(h.download()[0].tobytes()).hexdigest()[:16]
@@ -120,7 +120,7 @@ def c5(torch, stream, quick):
     t_max, t_min = aztec_extremal_states(order)
     h = DominoHandle(d, d.n + 1, 2 * count + 2)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.set_plan(ts.SweepPlan(d))
     masters = np.array([chain_master_seed(0x5EED, k) for k in range(count)], dtype=np.uint64)
     out = np.zeros((count, d.n + 1, d.n + 1), dtype=np.uint8)
     rr = np.zeros(count, dtype=np.int32)
@@ -162,7 +162,7 @@ def c4(torch, stream, quick):
     t_max, _ = aztec_extremal_states(order)
     h = DominoHandle(d, d.n + 1, 1)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.set_plan(ts.SweepPlan(d))
     h.upload(t_max[None])
     del t_max
     steps = 1024
@@ -190,7 +190,7 @@ def mixed(torch, stream, quick):
     t_max, _ = aztec_extremal_states(order)
     h = DominoHandle(d, d.n + 1, 1)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.set_plan(ts.SweepPlan(d))
     h.upload(t_max[None])
     tw = timed(torch, stream, lambda: h.walk([0x5EED], warm))
     st = h.download()[0]
@@ -219,7 +219,7 @@ def c5full(torch, stream, quick):
     t_max, t_min = aztec_extremal_states(order)
     h = DominoHandle(d, d.n + 1, 2 * count + 2)
     h.set_stream(stream.cuda_stream)
-    h.set_p_up(ts.SweepPlan(d).p_up)
+    h.set_plan(ts.SweepPlan(d))
     masters = np.array([chain_master_seed(0x5EED, k) for k in range(count)], dtype=np.uint64)
     out = np.zeros((count, d.n + 1, d.n + 1), dtype=np.uint8)
     rr = np.zeros(count, dtype=np.int32)
@@ -252,7 +252,7 @@ def strips(torch, stream, quick):
         t_max, _ = aztec_extremal_states(order)
         h = DominoHandle(d, d.n + 1, 1)
         h.set_stream(stream.cuda_stream)
-        h.set_p_up(ts.SweepPlan(d).p_up)
+        h.set_plan(ts.SweepPlan(d))
         h.upload(t_max[None])
         del t_max
         steps = 1024 if order <= 4096 else 256

@@ -12,7 +12,7 @@ world, halo, steps, order = (int(x) for x in sys.argv[1:5])
 d = ts.Domain.aztec(order); plan = ts.SweepPlan(d); t_max, _ = aztec_extremal_states(order)
 hs = []
 for _ in range(world):
-    h = DominoHandle(d, d.n + 1, 1, device=0); h.set_p_up(plan.p_up); h.upload(t_max[None]); hs.append(h)
+    h = DominoHandle(d, d.n + 1, 1, device=0); h.set_plan(plan); h.upload(t_max[None]); hs.append(h)
 bounds = strip_bounds(d.vertex_mask, world, min_rows=halo)
 print('bounds', bounds, flush=True)
 ws = DeviceStripWalker.local(hs, bounds, halo)

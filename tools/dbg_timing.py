@@ -9,7 +9,7 @@ from paper_1804_07250_b200.lattice import aztec_extremal_states
 from paper_1804_07250_b200.sweeps import DominoHandle
 rows = int(sys.argv[1]); order = 4096
 d = ts.Domain.aztec(order); t_max, _ = aztec_extremal_states(order)
-h = DominoHandle(d, d.n + 1, 1); h.set_p_up(ts.SweepPlan(d).p_up); h.upload(t_max[None])
+h = DominoHandle(d, d.n + 1, 1); h.set_plan(ts.SweepPlan(d)); h.upload(t_max[None])
 mid = (d.n + 1) // 2
 _native.check(_native.lib().tsb_domino_set_window(h._h, mid - rows // 2, mid + rows // 2))
 h.walk([1], 64); h.sync()

@@ -8,7 +8,7 @@ from paper_1804_07250_b200.lattice import aztec_extremal_states
 from paper_1804_07250_b200.sweeps import DominoHandle
 order = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 d = ts.Domain.aztec(order); t_max, _ = aztec_extremal_states(order)
-h = DominoHandle(d, d.n + 1, 1); h.set_p_up(ts.SweepPlan(d).p_up); h.upload(t_max[None])
+h = DominoHandle(d, d.n + 1, 1); h.set_plan(ts.SweepPlan(d)); h.upload(t_max[None])
 mid = (d.n + 1) // 2
 for rows in (8193, 4096, 2048, 1024, 512, 256, 128, 64, 24):
     lo, hi = max(0, mid - rows // 2), min(d.n + 1, mid + rows // 2)

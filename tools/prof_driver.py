@@ -56,7 +56,7 @@ def main():
         d = ts.Domain.aztec(n)
         t_max, _ = aztec_extremal_states(n)
         h = DominoHandle(d, d.n + 1, 1)
-        h.set_p_up(ts.SweepPlan(d).p_up)
+        h.set_plan(ts.SweepPlan(d))
         h.upload(t_max[None])
     h.walk([0x5EED], a.warm)
     h.walk([0x5EED], a.sweeps, step0=a.warm)
