@@ -148,6 +148,12 @@ int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, 
  * outside the domain stay 0.  density_map = acc / (#states added). */
 int tsb_domino_orientation_add(tsb_domino *h, int chain0, int n, uint32_t *acc_dev);
 
+/* Sample-archive record of chain `chain` (stats.py:146-153
+ * _serialize_state): the tilestates joined by single spaces in decimal, as one
+ * line without the newline, formatted on the device.  With out == NULL or
+ * cap < the record length only *len is set (size query). */
+int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t *len);
+
 /* ------------------------------------------------------------------ CFTP */
 /* Progress callback: (round, steps = sum_{i<=round} 2^i, samples collapsed so
  * far, batch size, user) -- the reference's progress hook (cftp.py:130-136). */
@@ -203,6 +209,9 @@ int tsb_sv_observe_add(tsb_sv *h, int chain0, int n, int observable, uint32_t *a
 /* Face heights summed into a device int64 accumulator ((n+1)^2): the mean
  * height function = acc / (#states added). */
 int tsb_sv_height_sum_add(tsb_sv *h, int chain0, int n, long long *acc_dev);
+/* Archive record: h_edges then v_edges ravelled as '0'/'1' (stats.py:146-153);
+ * size query as tsb_domino_serialize. */
+int tsb_sv_serialize(tsb_sv *h, int chain, char *out, size_t cap, size_t *len);
 int tsb_sv_coalesced(tsb_sv *h, int chain0, int npairs, uint8_t *flags);
 int tsb_sv_replicate(tsb_sv *h, int src, int dst0, int step, int n);
 /* sv_cftp (sixvertex.py:565-622): as tsb_domino_cftp with height grids. */
@@ -235,6 +244,8 @@ int tsb_loz_heights(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *out);
 /* loz_extremal (lozenge.py:762-775) into chains chain_max / chain_min;
  * TSB_E_UNTILEABLE when the domain has no tiling. */
 int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int ref_y);
+/* Archive record: edges (3, X, Y) ravelled as '0'/'1' (stats.py:146-153). */
+int tsb_loz_serialize(tsb_loz *h, int chain, char *out, size_t cap, size_t *len);
 int tsb_loz_coalesced(tsb_loz *h, int chain0, int npairs, uint8_t *flags);
 int tsb_loz_replicate(tsb_loz *h, int src, int dst0, int step, int n);
 /* loz_cftp (lozenge.py:778-827): as tsb_domino_cftp with edge grids. */

@@ -98,6 +98,9 @@ _SIGS = {
     "tsb_domino_extremal": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_orientation_add": (_i, [_vp, _i, _i, _vp]),
+    "tsb_domino_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
+    "tsb_sv_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
+    "tsb_loz_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
     "tsb_domino_strip_init": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_domino_strip_connect": (_i, [_vp, _vp, _vp]),
     "tsb_domino_strip_connect_local": (_i, [_vp, _vp, _vp]),

@@ -579,6 +579,17 @@ __global__ void __launch_bounds__(256) lz_coalesced(const uint4 *base, size_t ch
     if (threadIdx.x == 0) flags[j] = any ? 0 : 1;
 }
 
+// Archive record (stats.py:146-153): LozengeTiling.edges (3, X, Y) ravelled
+// as '0'/'1'; thread per (plane, row, 32-column word).
+__global__ void lz_serialize_kernel(const uint32_t *st, int X, int Y, int pitch, size_t plane, char *out) {
+    const int e = blockIdx.z, x = blockIdx.y, w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= X || w * 32 >= Y) return;
+    const uint32_t m = st[(size_t)e * plane + (size_t)(x + 1) * pitch + w];
+    char *o = out + ((size_t)e * X + x) * Y + (size_t)w * 32;
+    const int lim = min(32, Y - w * 32);
+    for (int b = 0; b < lim; ++b) o[b] = ((m >> b) & 1u) ? '1' : '0';
+}
+
 // ----------------------------------------------------------------- host helpers
 int lz_check(tsb_loz *h, int chain0, int n) {
     if (!h) return fail(TSB_E_VALUE, "null handle");
@@ -1051,6 +1062,26 @@ int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int re
     cudaFree(df);
     if (rc) return rc;
     if (untileable) return fail(TSB_E_UNTILEABLE, "triangle domain is not tileable");
+    return TSB_OK;
+}
+
+int tsb_loz_serialize(tsb_loz *h, int chain, char *out, size_t cap, size_t *len) {
+    if (!h || !len) return fail(TSB_E_VALUE, "null argument");
+    int rc = lz_check(h, chain, 1);
+    if (rc) return rc;
+    const size_t total = 3 * (size_t)h->X * h->Y;
+    *len = total;
+    if (!out || cap < total) return TSB_OK;  // size query
+    TSB_CUDA(cudaSetDevice(h->device));
+    char *d = nullptr;
+    TSB_CUDA(cudaMalloc(&d, total));
+    lz_serialize_kernel<<<dim3((h->W + 63) / 64, h->X, 3), 64, 0, h->stream>>>(
+        h->buf[h->cur] + (size_t)chain * h->chain_words, h->X, h->Y, h->pitch, h->plane, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "loz serialize");
     return TSB_OK;
 }
 

@@ -692,6 +692,20 @@ __global__ void sv_height_sum_kernel(const int32_t *h, int nchains, size_t nf, l
     acc[i] += s;
 }
 
+// Archive record (stats.py:146-153): h_edges (n, n+1) then v_edges (n+1, n)
+// ravelled as '0'/'1' characters; thread per (row, 32-site word).
+__global__ void sv_serialize_kernel(const uint32_t *bits, int p0, int pitch, int n, char *out) {
+    const int part = blockIdx.z;  // 0: h_edges, 1: v_edges
+    const int rows = part ? n + 1 : n, cols = part ? n : n + 1;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (r >= rows || w * 32 >= cols) return;
+    const uint32_t *row = bits + pitch + (size_t)r * pitch;  // face row r (after the guard row)
+    const uint32_t m = part ? sv_vedge(row, w, r, p0) : sv_hedge(row, row + pitch, w, r, p0);
+    char *o = out + (part ? (size_t)n * (n + 1) : 0) + (size_t)r * cols + (size_t)w * 32;
+    const int lim = min(32, cols - w * 32);
+    for (int b = 0; b < lim; ++b) o[b] = ((m >> b) & 1u) ? '1' : '0';
+}
+
 int sv_check(tsb_sv *h, int chain0, int n) {
     if (!h) return fail(TSB_E_VALUE, "null handle");
     if (chain0 < 0 || n < 0 || chain0 + n > h->nchains)
@@ -986,6 +1000,30 @@ int tsb_sv_height_sum_add(tsb_sv *h, int chain0, int n, long long *acc_dev) {
     const size_t nf = (size_t)h->f * h->f;
     sv_height_sum_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, h->stream>>>(h->hbuf, n, nf, acc_dev);
     TSB_CUDA(cudaGetLastError());
+    return TSB_OK;
+}
+
+int tsb_sv_serialize(tsb_sv *h, int chain, char *out, size_t cap, size_t *len) {
+    if (!h || !len) return fail(TSB_E_VALUE, "null argument");
+    int rc = sv_check(h, chain, 1);
+    if (rc) return rc;
+    const size_t total = 2 * (size_t)h->n * (h->n + 1);
+    *len = total;
+    if (!out || cap < total) return TSB_OK;  // size query
+    TSB_CUDA(cudaSetDevice(h->device));
+    int32_t p00 = 0;
+    TSB_CUDA(cudaMemcpyAsync(&p00, h->h00 + chain, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    char *d = nullptr;
+    TSB_CUDA(cudaMalloc(&d, total));
+    const int W = (h->n + 1 + 31) / 32;
+    sv_serialize_kernel<<<dim3((W + 63) / 64, h->n + 1, 2), 64, 0, h->stream>>>(
+        h->bits + (size_t)chain * h->chain_words, p00 & 1, h->pitch, h->n, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "sv serialize");
     return TSB_OK;
 }
 

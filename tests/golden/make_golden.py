@@ -255,7 +255,46 @@ def make_observables():
     save("observables.npz", **arrays)
 
 
+# ------------------------------------------------------------- archives
+def make_archives():
+    """stats.SampleArchive text (create + extend + dump, stats.py:75-153) of
+    reference-sampled states of each model, with the states themselves."""
+    import io
+
+    from tilesampler import stats
+
+    arrays = {}
+    d = ts.Domain.aztec(12)
+    t_max, _ = ts.extremal_tilings(d)
+    st = ts.random_walk_batch(np.stack([t_max.states] * 3), np.array([1, 2, 3], dtype=np.uint64), 60,
+                              ts.SweepPlan(d))
+    n = 8
+    b = ts.dwbc(n)
+    lo = ts.sv_extremal(n, b)[1]
+    hs = sv_random_walk_batch(np.stack([lo.heights] * 3), np.array([4, 5, 6], dtype=np.uint64), 50,
+                              ts.SVWeights(1.0, 1.0, 1.2))
+    dom = ts.TriDomain.hexagon(3, 4, 5)
+    t_max_l, _ = ts.loz_extremal(dom)
+    es = loz_random_walk_batch(np.stack([t_max_l.edges] * 3), np.array([7, 8, 9], dtype=np.uint64), 50, dom,
+                               ts.Uniform())
+    cases = {
+        "domino": (d, [ts.Tiling(d, s) for s in st]),
+        "sixvertex": (b, [ts.config_from_heights(ts.FaceHeights(n, h)) for h in hs]),
+        "lozenge": (dom, [LozengeTiling(dom, e) for e in es]),
+    }
+    arrays.update(dom_states=st, sv_heights=hs, loz_edges=es)
+    for model, (domain, states) in cases.items():
+        arc = stats.SampleArchive.create(model, domain, "uniform", 0x5EED, "sequential", "mcmc steps=60")
+        arc.extend(states)
+        buf = io.StringIO()
+        arc.dump(buf)
+        with open(os.path.join(HERE, f"archive_{model}.txt"), "w") as fh:
+            fh.write(buf.getvalue())
+        print(f"archive {model}: {len(buf.getvalue())} chars")
+    save("archives.npz", **arrays)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables"]
+    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables", "archives"]
     for w in which:
         globals()[f"make_{w}"]()
