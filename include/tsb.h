@@ -47,6 +47,11 @@ enum {
 const char *tsb_last_error(void);
 int tsb_abi_version(void);
 /* SM count, compute capability and L2 size of `device`. */
+/* Number of 4-connected components of the nonzero cells of a (rows x cols)
+ * uint8 grid (GPU union-find): the Domain checks of lattice.py:99-132
+ * (faces connected <=> 1 component; no hole <=> the complement padded by one
+ * ring of cells is 1 component) without the reference's Python DFS. */
+int tsb_grid_components(int device, const uint8_t *grid, int rows, int cols, int64_t *ncomp);
 int tsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor, int64_t *l2_bytes);
 
 /* ------------------------------------------------------------------- RNG */

@@ -78,6 +78,7 @@ _SIGS = {
     "tsb_last_error": (ctypes.c_char_p, []),
     "tsb_abi_version": (_i, []),
     "tsb_device_info": (_i, [_i, _vp, _vp, _vp, _vp]),
+    "tsb_grid_components": (_i, [_i, _vp, _i, _i, _vp]),
     "tsb_uniform_grid": (_i, [_i, _u64, _i, _i, _u64, _i, _vp]),
     "tsb_domino_create": (_i, [_i, _i, _i, _vp, _vp]),
     "tsb_domino_destroy": (_i, [_vp]),
@@ -199,3 +200,20 @@ def ptr(a: np.ndarray):
 
 def u64(x: int) -> int:
     return int(x) & 0xFFFFFFFFFFFFFFFF
+
+
+_has_device = None
+
+
+def has_device() -> bool:
+    """True when libtsb loads and sees an sm_100 device (no exception)."""
+    global _has_device
+    if _has_device is None:
+        try:
+            sm = ctypes.c_int()
+            major = ctypes.c_int()
+            _has_device = lib().tsb_device_info(0, ctypes.byref(sm), ctypes.byref(major), None, None) == OK \
+                and major.value == 10
+        except Exception:
+            _has_device = False
+    return _has_device

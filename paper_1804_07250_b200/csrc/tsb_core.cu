@@ -54,6 +54,55 @@ __global__ void uniform_grid_kernel(uint64_t base, int64_t count, uint64_t tag, 
     out[i] = (double)(draw(key, step) >> 11) * 0x1p-53;
 }
 
+// Connected components of a cell grid (4-neighbourhood) by lock-free
+// union-find (Domain validation, lattice.py:99-132,
+// whose DFS is O(n^2) pure Python).  label[i] = parent index, -1 outside.
+__device__ __forceinline__ int uf_find(const int *L, int x) {
+    int p = L[x];
+    while (p != x) {
+        x = p;
+        p = L[x];
+    }
+    return x;
+}
+
+__device__ void uf_unite(int *L, int a, int b) {
+    for (;;) {
+        a = uf_find(L, a);
+        b = uf_find(L, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        // link the larger root under the smaller one; retry if b was re-linked meanwhile
+        const int old = atomicCAS(&L[b], b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void cc_init(const uint8_t *grid, int64_t n, int *L) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) L[i] = grid[i] ? (int)i : -1;
+}
+
+__global__ void cc_merge(int rows, int cols, int *L) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)rows * cols || L[i] < 0) return;
+    const int c = (int)(i % cols);
+    if (c + 1 < cols && L[i + 1] >= 0) uf_unite(L, (int)i, (int)(i + 1));
+    if (i + cols < (int64_t)rows * cols && L[i + cols] >= 0) uf_unite(L, (int)i, (int)(i + cols));
+}
+
+__global__ void cc_count_roots(const int *L, int64_t n, unsigned long long *count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int root = i < n && L[i] == (int)i;
+    const unsigned long long k = __popc(__ballot_sync(0xffffffffu, root));
+    if ((threadIdx.x & 31) == 0 && k) atomicAdd(count, k);
+}
+
 }  // namespace tsb
 
 using namespace tsb;
@@ -63,6 +112,37 @@ extern "C" {
 const char *tsb_last_error(void) { return g_err.c_str(); }
 
 int tsb_abi_version(void) { return 1; }
+
+int tsb_grid_components(int device, const uint8_t *grid, int rows, int cols, int64_t *ncomp) {
+    if (!grid || !ncomp || rows < 1 || cols < 1) return fail(TSB_E_VALUE, "bad grid arguments");
+    const int64_t n = (int64_t)rows * cols;
+    if (n >= (1ll << 31)) return fail(TSB_E_CAPACITY, "grid of %lld cells exceeds 2^31", (long long)n);
+    int rc = ensure_device(device);
+    if (rc) return rc;
+    uint8_t *dg = nullptr;
+    int *L = nullptr;
+    unsigned long long *dc = nullptr;
+    cudaError_t e = cudaMalloc(&dg, n);
+    if (e == cudaSuccess) e = cudaMalloc(&L, sizeof(int) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&dc, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemcpy(dg, grid, n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dc, 0, sizeof(unsigned long long));
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (e == cudaSuccess) {
+        cc_init<<<blocks, 256>>>(dg, n, L);
+        cc_merge<<<blocks, 256>>>(rows, cols, L);
+        cc_count_roots<<<blocks, 256>>>(L, n, dc);
+        e = cudaGetLastError();
+    }
+    unsigned long long k = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&k, dc, sizeof k, cudaMemcpyDeviceToHost);
+    cudaFree(dg);
+    cudaFree(L);
+    cudaFree(dc);
+    if (e != cudaSuccess) return cuda_fail(e, "grid components");
+    *ncomp = (int64_t)k;
+    return TSB_OK;
+}
 
 int tsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor, int64_t *l2_bytes) {
     int n = 0;
