@@ -24,6 +24,7 @@
 // out of place (double buffer).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "domino.cuh"
@@ -241,6 +242,61 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     TT(5);
 }
 
+// The same temporal blocking with ONE {V,H} word per lane (tiles of 30 output
+// words): chosen for narrow lattices (e.g. CFTP at Aztec 512, W = 33 words),
+// where the 62-word tiles would leave half of every warp outside the domain.
+// Lanes 0 and 31 hold the halo words.
+template <int TM>
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx c) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t(*vs)[32] = reinterpret_cast<uint32_t(*)[32]>(dsm);
+    uint32_t(*fs)[32] = reinterpret_cast<uint32_t(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
+    uint32_t(*fres)[64] = reinterpret_cast<uint32_t(*)[64]>(dsm + 2 * sizeof(uint2) * kMRows * 32);
+    uint16_t(*queue)[1024] =
+        reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64);
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
+    const int r = tile.y * kMOut - kMK + k;
+    const int wa = tile.x + lane;  // tile.x = first loaded word
+    const int z = blockIdx.z;
+    const bool in_grid = r >= 0 && r < c.side;
+    const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint2 cur = make_uint2(0u, 0u);
+    if (in_grid) cur = __ldg(row + wa);
+    const uint64_t step0 = *c.step_dev + c.step;
+    const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;
+#pragma unroll 1
+    for (int s = 0; s < kMK; ++s) {
+        const uint64_t step = step0 + (uint64_t)s;
+        const int color = c.colors[z * kGraphSweeps + (int)c.step + s];
+        vs[k][lane] = cur.x;
+        __syncthreads();
+        const uint32_t vu = k > 0 ? vs[k - 1][lane] : 0u;
+        const uint32_t act = color ? ~act0 : act0;
+        const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.y, 1);  // lane 0: halo, wraps harmlessly
+        const uint32_t la = (cur.y << 1) | (hl >> 31);
+        const uint32_t ia = vu & cur.x & ~(la | cur.y);
+        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act;
+        uint32_t f = 0u;
+        if (__any_sync(0xffffffffu, ra != 0u)) {
+            const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
+            f = warp_fire<TM, 1>(ra, 0u, ia, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step).x;
+        }
+        fs[k][lane] = f;
+        __syncthreads();
+        const uint32_t fn = k + 1 < kMRows ? fs[k + 1][lane] : 0u;  // F(r+1)
+        const uint32_t fr = __shfl_down_sync(0xffffffffu, f, 1);
+        cur = make_uint2(cur.x ^ f ^ fn, cur.y ^ f ^ (f >> 1) ^ (fr << 31));
+    }
+    if (k >= kMK && k < kMRows - kMK && in_grid && lane > 0 && lane < 31) {
+        uint2 *out = c.dst + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+        out[wa] = cur;
+    }
+}
+
 // Colours of the next kGraphSweeps sweeps of every chain (graph mode).
 __global__ void colors_kernel(const uint64_t *seedinfo, const uint64_t *step_dev, uint64_t offset,
                               uint8_t *colors) {
@@ -443,6 +499,14 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (h->m_wpl == 1) {
+        switch (h->tmode) {
+            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<0>, c)); break;
+            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<1>, c)); break;
+            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<2>, c)); break;
+        }
+        return TSB_OK;
+    }
     switch (h->tmode) {
         case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<0>, c)); break;
         case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<1>, c)); break;
@@ -611,17 +675,37 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         // multi-sweep tiles are aligned to each band's own word range: tile.x
         // = first loaded word wa0 (even, for 16-byte loads), outputs words
         // wa0+1 .. wa0+kTileWords; a band [wl, wh) starts at (wl-1) & ~1
+        // Two widths: 2 words per lane (62 output words, 16-byte loads) or 1
+        // (30 output words) -- whichever covers the domain with fewer word
+        // slots (TSB_DOM_WPL=1|2 forces one).
         const int nb = (side + kMOut - 1) / kMOut;
-        h->mband_start.assign(nb + 1, 0);
-        for (int y = 0; y < nb; ++y) {
-            h->mband_start[y] = (int)mtiles.size();
-            int lo = INT_MAX, hi = INT_MIN;
-            for (int r = y * kMOut; r < std::min(side, (y + 1) * kMOut); ++r)
-                if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
-            if (hi <= lo) continue;
-            for (int wa0 = (lo - 1) & ~1; wa0 + 1 < hi; wa0 += kTileWords) mtiles.push_back(make_int2(wa0, y));
+        auto build = [&](int wpl, std::vector<int2> &tl, std::vector<int> &bs) {
+            const int out_words = 32 * wpl - 2;
+            bs.assign(nb + 1, 0);
+            for (int y = 0; y < nb; ++y) {
+                bs[y] = (int)tl.size();
+                int lo = INT_MAX, hi = INT_MIN;
+                for (int r = y * kMOut; r < std::min(side, (y + 1) * kMOut); ++r)
+                    if (rg[r].y > rg[r].x) { lo = std::min(lo, rg[r].x); hi = std::max(hi, rg[r].y); }
+                if (hi <= lo) continue;
+                for (int wa0 = wpl == 2 ? ((lo - 1) & ~1) : lo - 1; wa0 + 1 < hi; wa0 += out_words)
+                    tl.push_back(make_int2(wa0, y));
+            }
+            bs[nb] = (int)tl.size();
+        };
+        std::vector<int2> t1;
+        std::vector<int> b1, b2;
+        build(2, mtiles, b2);
+        build(1, t1, b1);
+        int wpl = (size_t)t1.size() * 32 < mtiles.size() * 64 * 9 / 10 ? 1 : 2;  // 1 only when clearly cheaper
+        if (const char *ev = getenv("TSB_DOM_WPL")) wpl = atoi(ev) == 1 ? 1 : 2;
+        h->m_wpl = wpl;
+        if (wpl == 1) {
+            mtiles.swap(t1);
+            h->mband_start.swap(b1);
+        } else {
+            h->mband_start.swap(b2);
         }
-        h->mband_start[nb] = (int)mtiles.size();
     }
     h->ntiles = (int)tiles.size();
     h->nmtiles = (int)mtiles.size();
@@ -635,7 +719,8 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         (e = cudaMemcpy(h->mtiles, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
         return bail(e, "mtiles");
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
-                           (const void *)domino_multi_kernel<2>})
+                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
+                           (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem)) != cudaSuccess)
             return bail(e, "smem attribute");
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)

@@ -21,6 +21,7 @@ struct tsb_domino {
     int nmtiles = 0;
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
+    int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;

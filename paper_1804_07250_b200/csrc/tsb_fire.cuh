@@ -7,9 +7,10 @@
 namespace tsb {
 
 // Heat-bath coins of a warp's rotateable active vertices, load-balanced.
-// Each lane owns two words (bits `ra`, `rb` rotateable; `ia`, `ib`: the site
+// Each lane owns WPL (1 or 2) words (bits `ra`, `rb` rotateable, rb = 0 when
+// WPL = 1; `ia`, `ib`: the site
 // fires iff (u < p) equals this bit -- domino state 3, lozenge ROT_LOW).
-// Site index = r * side + 32 * word + bit, word = wa - 2 * lane + 2 * lane'.
+// Site index = r * side + 32 * word + bit, word = wa - WPL * lane + WPL * lane'.
 // The warp's sites are queued in shared memory and dealt round-robin to the
 // lanes, two independent splitmix64 chains per lane per iteration, so a word
 // full of rotateable sites no longer serialises its lane (dense mixed states).
@@ -17,7 +18,7 @@ namespace tsb {
 // (_kernels.py:49-55, sweeps.py:102-110); a lozenge star moves to the high
 // state when u < p (lozenge.py:575-597).  Only rotateable sites are drawn and
 // counter-based draws make the skipping exact.
-template <int TM>
+template <int TM, int WPL = 2>
 __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, uint32_t ib, uint16_t *queue,
                                         uint32_t *fres, const uint64_t *__restrict__ seedinfo,
                                         const uint64_t *__restrict__ tgrid, uint64_t t, int side, int z, int r,
@@ -46,18 +47,19 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     __syncwarp();
     const uint64_t base = seedinfo[2 * z];
     const uint64_t salt = (step + 1ull) * kGold;
-    // site index r * side + column; column = 32 * (wa of lane 0) + 64 * lane + 32 * word + bit
-    const uint64_t row_idx = (uint64_t)r * (uint64_t)side + (uint64_t)(int64_t)((wa - 2 * lane) * 32);
+    // site index r * side + column; column = 32 * (wa of lane 0) + 32 * WPL * lane + 32 * word + bit
+    const uint64_t row_idx = (uint64_t)r * (uint64_t)side + (uint64_t)(int64_t)((wa - WPL * lane) * 32);
     for (int j = lane; j < total; j += 64) {
         const bool two = j + 32 < total;
         const uint32_t q0 = queue[j], q1 = two ? queue[j + 32] : q0;
-        const uint64_t i0 = row_idx + (uint64_t)(q0 & 63u) + (uint64_t)(((q0 >> 6) & 31u) * 64u);
-        const uint64_t i1 = row_idx + (uint64_t)(q1 & 63u) + (uint64_t)(((q1 >> 6) & 31u) * 64u);
+        const uint64_t i0 = row_idx + (uint64_t)(q0 & 63u) + (uint64_t)(((q0 >> 6) & 31u) * (32u * WPL));
+        const uint64_t i1 = row_idx + (uint64_t)(q1 & 63u) + (uint64_t)(((q1 >> 6) & 31u) * (32u * WPL));
         // two independent chains for ILP
         const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
         const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
         const uint64_t t0 = TM == 2 ? __ldg(tgrid + i0) : t;
         const uint64_t t1 = TM == 2 ? __ldg(tgrid + i1) : t;
+        // fire word of (lane', word) = fres[2 * lane' + word] (WPL = 1: word 0 only)
         if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
         if (two && ((x1 >> 11) < t1) == (bool)(q1 >> 11)) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
     }

@@ -291,3 +291,31 @@ def test_c4_size_walk_windows_vs_oracle():
         rows = np.ascontiguousarray(t_max[lo:hi])
         oracle.domino_walk_window(rows, lo, 0x5EED, np.full((hi - lo, side), 0.5), steps)
         assert np.array_equal(rows[a - lo:b - lo], out[a:b]), (a, b)
+
+
+@pytest.mark.parametrize("wpl", [1, 2])
+def test_golden_walks_both_tile_widths(monkeypatch, wpl):
+    """Every golden walk case with the multi-sweep tiles forced to 1 and to 2
+    words per lane (the library picks per lattice; both must be exact)."""
+    monkeypatch.setenv("TSB_DOM_WPL", str(wpl))
+    g = np.load(os.path.join(G, "domino_walks.npz"))
+    i = 0
+    while f"c{i}_faces" in g:
+        d = ts.Domain(g[f"c{i}_faces"].shape[0], g[f"c{i}_faces"])
+        start = g[f"c{i}_start"]
+        h = DominoHandle(d, d.n + 1, start.shape[0])
+        h.set_p_up(g[f"c{i}_p_up"])
+        h.upload(start)
+        h.walk(g[f"c{i}_seeds"], int(g[f"c{i}_n_steps"]))
+        assert np.array_equal(h.download(), g[f"c{i}_out"]), f"case {i} wpl {wpl}"
+        i += 1
+    for order, steps in ((200, 333), (700, 130)):
+        d = ts.Domain.aztec(order)
+        plan = ts.SweepPlan(d)
+        t_max, t_min = ts.extremal_tilings(d)
+        start = np.stack([t_max.states, t_min.states])
+        h = DominoHandle(d, d.n + 1, 2)
+        h.set_plan(plan)
+        h.upload(start)
+        h.walk([5, 6], steps)
+        assert np.array_equal(h.download(), oracle.domino_walk(start, [5, 6], plan.p_up, steps)), (order, wpl)
