@@ -111,7 +111,10 @@ int tsb_domino_cftp(tsb_domino *h, const uint8_t *top0, const uint8_t *bot0, con
             seeds.assign(2 * na, 0);
             for (int j = 0; j < na; ++j)
                 seeds[2 * j] = seeds[2 * j + 1] = derive_seed(masters[active[j]], (uint64_t)i, kSeedSalt);
-            if ((rc = tsb_domino_walk(h, 0, 2 * na, seeds.data(), 0, 1ull << i))) return rc;
+            h->coupled = true;  // pairs share seeds: draw each coin once per pair
+            rc = tsb_domino_walk(h, 0, 2 * na, seeds.data(), 0, 1ull << i);
+            h->coupled = false;
+            if (rc) return rc;
         }
         flags.assign(na, 0);
         if ((rc = tsb_domino_coalesced(h, 0, na, flags.data()))) return rc;

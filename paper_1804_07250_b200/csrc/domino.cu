@@ -297,6 +297,78 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
     }
 }
 
+// CFTP's coupled pairs (cftp.py:115-119): chains 2z and 2z+1 run from T_max /
+// T_min with the SAME seeds, so every coin is shared.  One block sweeps the
+// tile in both chains and draws each coin once, for the union of the two
+// chains' rotateable sites: with c = (u < p_up), a site fires in a chain iff
+// it is rotateable there and c equals its "state 3" bit -- exactly what two
+// independent sweeps compute.  Narrow (1 word per lane) tiles.
+template <int TM>
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx c) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t(*vs)[kMRows][32] = reinterpret_cast<uint32_t(*)[kMRows][32]>(dsm);
+    uint32_t(*fs)[kMRows][32] = reinterpret_cast<uint32_t(*)[kMRows][32]>(dsm + 2 * sizeof(uint32_t) * kMRows * 32);
+    uint32_t(*fres)[64] = reinterpret_cast<uint32_t(*)[64]>(dsm + 2 * sizeof(uint2) * kMRows * 32);
+    uint16_t(*queue)[1024] =
+        reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64);
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
+    const int r = tile.y * kMOut - kMK + k;
+    const int wa = tile.x + lane;
+    const int zt = 2 * blockIdx.z;  // top chain; bottom = zt + 1
+    const bool in_grid = r >= 0 && r < c.side;
+    const uint2 *rowt = c.src + (size_t)zt * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    const uint2 *rowb = rowt + c.chain_stride;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint2 ct = make_uint2(0u, 0u), cb = make_uint2(0u, 0u);
+    if (in_grid) {
+        ct = __ldg(rowt + wa);
+        cb = __ldg(rowb + wa);
+    }
+    const uint64_t step0 = *c.step_dev + c.step;
+    const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;
+#pragma unroll 1
+    for (int s = 0; s < kMK; ++s) {
+        const uint64_t step = step0 + (uint64_t)s;
+        const int color = c.colors[zt * kGraphSweeps + (int)c.step + s];
+        vs[0][k][lane] = ct.x;
+        vs[1][k][lane] = cb.x;
+        __syncthreads();
+        const uint32_t vut = k > 0 ? vs[0][k - 1][lane] : 0u, vub = k > 0 ? vs[1][k - 1][lane] : 0u;
+        const uint32_t act = color ? ~act0 : act0;
+        const uint32_t hlt = __shfl_up_sync(0xffffffffu, ct.y, 1), hlb = __shfl_up_sync(0xffffffffu, cb.y, 1);
+        const uint32_t lat = (ct.y << 1) | (hlt >> 31), lab = (cb.y << 1) | (hlb >> 31);
+        const uint32_t iat = vut & ct.x & ~(lat | ct.y), iab = vub & cb.x & ~(lab | cb.y);
+        const uint32_t rat = (iat | (~(vut | ct.x) & lat & ct.y)) & act;
+        const uint32_t rab = (iab | (~(vub | cb.x) & lab & cb.y)) & act;
+        const uint32_t un = rat | rab;
+        uint32_t ft = 0u, fb = 0u;
+        if (__any_sync(0xffffffffu, un != 0u)) {
+            const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
+            // coin bits: 1 where u < p_up, on the union of both chains' sites
+            const uint32_t cu =
+                warp_fire<TM, 1>(un, 0u, 0xFFFFFFFFu, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, zt, r,
+                                 wa, step).x;
+            ft = rat & ~(cu ^ iat);
+            fb = rab & ~(cu ^ iab);
+        }
+        fs[0][k][lane] = ft;
+        fs[1][k][lane] = fb;
+        __syncthreads();
+        const uint32_t fnt = k + 1 < kMRows ? fs[0][k + 1][lane] : 0u, fnb = k + 1 < kMRows ? fs[1][k + 1][lane] : 0u;
+        const uint32_t frt = __shfl_down_sync(0xffffffffu, ft, 1), frb = __shfl_down_sync(0xffffffffu, fb, 1);
+        ct = make_uint2(ct.x ^ ft ^ fnt, ct.y ^ ft ^ (ft >> 1) ^ (frt << 31));
+        cb = make_uint2(cb.x ^ fb ^ fnb, cb.y ^ fb ^ (fb >> 1) ^ (frb << 31));
+    }
+    if (k >= kMK && k < kMRows - kMK && in_grid && lane > 0 && lane < 31) {
+        uint2 *out = c.dst + (size_t)zt * c.chain_stride + (ptrdiff_t)r * c.pitch;
+        out[wa] = ct;
+        out[wa + c.chain_stride] = cb;
+    }
+}
+
 // Colours of the next kGraphSweeps sweeps of every chain (graph mode).
 __global__ void colors_kernel(const uint64_t *seedinfo, const uint64_t *step_dev, uint64_t offset,
                               uint8_t *colors) {
@@ -499,6 +571,15 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (h->m_wpl == 1 && h->coupled && (n & 1) == 0) {
+        cfg.gridDim.z = n / 2;  // one block per tile and coupled pair
+        switch (h->tmode) {
+            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<0>, c)); break;
+            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<1>, c)); break;
+            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<2>, c)); break;
+        }
+        return TSB_OK;
+    }
     if (h->m_wpl == 1) {
         switch (h->tmode) {
             case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<0>, c)); break;
@@ -526,7 +607,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
                       h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
                       h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0 &&
-                      h->g_tail == h->graph_tail;
+                      h->g_tail == h->graph_tail && h->g_coupled == h->coupled;
     if (same) return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -563,6 +644,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_winn = h->win_tn;
     h->g_winm = h->win_m0;
     h->g_tail = h->graph_tail;
+    h->g_coupled = h->coupled;
     return TSB_OK;
 }
 
@@ -720,7 +802,9 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         return bail(e, "mtiles");
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
                            (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
-                           (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>})
+                           (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>,
+                           (const void *)domino_multi1c_kernel<0>, (const void *)domino_multi1c_kernel<1>,
+                           (const void *)domino_multi1c_kernel<2>})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem)) != cudaSuccess)
             return bail(e, "smem attribute");
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)

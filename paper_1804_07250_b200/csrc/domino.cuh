@@ -22,6 +22,7 @@ struct tsb_domino {
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
+    bool coupled = false, g_coupled = false;  // chains 2j, 2j+1 share seeds (CFTP pairs): share the coins
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;
