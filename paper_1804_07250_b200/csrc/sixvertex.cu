@@ -275,37 +275,7 @@ __global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
             se[j] = ((d[j] >> 1) | (nd << 31)) ^ b[j];
             cnt += __popc(cand[j]);
         }
-        const int maxc = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
-        if (maxc != 0 && maxc <= 4) {
-            // sparse: every lane draws its own candidates, two chains at a time
-            const uint64_t salt = (step0 + (uint64_t)s + 1ull) * kGold;
-            const uint64_t row_idx = (uint64_t)R * (uint64_t)c.f;
-#pragma unroll
-            for (int j = 0; j < WPL; ++j) {
-                uint32_t m = cand[j], fl = 0u;
-                const uint64_t widx = row_idx + (uint64_t)(int64_t)((wl + j) * 32);
-                while (m) {
-                    const int b0 = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int b1 = m ? __ffs(m) - 1 : b0;
-                    m &= m - 1;
-                    const uint64_t x0 = mix64(mix64(base + (widx + (uint64_t)b0 + 1ull) * kGold) + salt);
-                    const uint64_t x1 = mix64(mix64(base + (widx + (uint64_t)b1 + 1ull) * kGold) + salt);
-                    const uint32_t li0 = (((mn[j] >> b0) & 1u) ? 0u : 16u) | (((nw[j] >> b0) & 1u) << 3) |
-                                         (((ne[j] >> b0) & 1u) << 2) | (((sw[j] >> b0) & 1u) << 1) | ((se[j] >> b0) & 1u);
-                    const uint32_t li1 = (((mn[j] >> b1) & 1u) ? 0u : 16u) | (((nw[j] >> b1) & 1u) << 3) |
-                                         (((ne[j] >> b1) & 1u) << 2) | (((sw[j] >> b1) & 1u) << 1) | ((se[j] >> b1) & 1u);
-                    if (((x0 >> 11) < lut[li0]) == !(li0 & 16u)) fl |= 1u << b0;
-                    if (((x1 >> 11) < lut[li1]) == !(li1 & 16u)) fl |= 1u << b1;
-                }
-                if (fl) {
-                    const uint32_t nb = b[j] ^ fl;
-                    if (pr == 0) ra[j] = nb;
-                    else rb[j] = nb;
-                    rows[i][lane * WPL + j] = nb;
-                }
-            }
-        } else if (maxc != 0) {
+        if (__any_sync(0xffffffffu, cnt != 0)) {
             int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
