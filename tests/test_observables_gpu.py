@@ -135,3 +135,35 @@ def test_arctic_circle_statistics():
     assert abs(float(np.nanmean(grid[centre])) - 0.5) < 0.05
     y = float(np.mean(yints))
     assert abs(y + order / np.sqrt(2.0)) < 0.12 * order / np.sqrt(2.0), y
+
+
+def test_sixvertex_free_fermion_arctic_circle():
+    """Statistical observable where draws cannot be matched: DWBC six-vertex at
+    the free-fermion point (a = b = 1, c = sqrt 2, Delta = 0) has the arctic
+    circle inscribed in the square; outside 1.1x its radius the four corners
+    are frozen (every edge-occupancy density within 0.05 of 0 or 1), inside
+    0.5x the edges fluctuate.  Device densities over 16 chains x 8 samples."""
+    import math
+
+    n, chains = 96, 16
+    R, C = np.meshgrid(np.arange(n + 1), np.arange(n + 1), indexing="ij")
+    lo = np.maximum(-(R + C), R + C - 2 * n).astype(np.int32)
+    h = SixVertexHandle(n, chains)
+    h.set_weights(ts.SVWeights(1.0, 1.0, math.sqrt(2.0)))
+    h.upload(np.stack([lo] * chains))
+    seeds = np.arange(50, 50 + chains, dtype=np.uint64)
+    burn = 40 * n * n
+    h.walk(seeds, burn)
+    acc = DeviceDensity(h, "h-edge")
+    step = burn
+    for _ in range(8):
+        h.walk(seeds, 2 * n * n, step0=step)
+        step += 2 * n * n
+        acc.add()
+    grid = acc.result().grid  # (n, n+1): h_edges[r, c] between faces (r, c), (r+1, c)
+    rr, cc = np.meshgrid(np.arange(n) + 1.0 - (n + 1) / 2, np.arange(n + 1) + 0.5 - (n + 1) / 2, indexing="ij")
+    rad = np.hypot(rr, cc)
+    frozen = grid[rad > 1.1 * n / 2]
+    assert np.minimum(frozen, 1 - frozen).max() < 0.05, np.minimum(frozen, 1 - frozen).max()
+    inner = grid[rad < 0.5 * n / 2]
+    assert 0.2 < inner.mean() < 0.8 and np.minimum(inner, 1 - inner).mean() > 0.15
