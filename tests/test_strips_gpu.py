@@ -133,3 +133,27 @@ def test_device_strips_ipc_processes(tmp_path, world, halo):
     ref = oracle_walk(t_max, ts.SweepPlan(d).p_up, steps, 0)
     got = np.concatenate([np.load(tmp_path / f"dstrip{r}.npy") for r in range(world)])
     assert np.array_equal(got, ref)
+
+
+def _cftp_worker(rank, world, port, out_dir):
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.cftp import cftp_sample_many_distributed
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    d = ts.Domain.aztec(10)
+    res = cftp_sample_many_distributed(d, ts.SweepPlan(d), 0xC0FFEE, 7)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "cftp.npy"), np.stack([t.states for t in res]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_cftp_samples_spread_over_processes(tmp_path):
+    """CFTP samples distributed round-robin over ranks equal the one-GPU run."""
+    import paper_1804_07250_b200 as ts
+
+    mp.spawn(_cftp_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    d = ts.Domain.aztec(10)
+    ref = np.stack([t.states for t in ts.cftp_sample_many(d, ts.SweepPlan(d), 0xC0FFEE, 7)])
+    assert np.array_equal(np.load(tmp_path / "cftp.npy"), ref)
