@@ -120,3 +120,37 @@ def test_multi_sweep_vs_oracle(monkeypatch, K, abc, w, steps):
     h.upload(start)
     h.walk(seeds, steps)
     assert np.array_equal(h.download(), oracle.loz_walk(start, seeds, p, steps))
+
+
+def test_hexagon_arctic_circle_statistics():
+    """Statistical observable where draws cannot be matched: uniform lozenge
+    tilings of the regular hexagon (side m) are frozen outside the inscribed
+    circle (Cohn-Larsen-Propp).  With the axial lattice embedded as
+    P(x, y) = x (1, 0) + y (1/2, sqrt3/2) (DIRS, lozenge.py:43), every edge
+    family's crossing density is within 0.05 of 0 or 1 beyond 1.1x the
+    inradius m sqrt3/2 and near 1/3 inside half of it."""
+    m, chains = 64, 16
+    d = ts.TriDomain.hexagon(m, m, m)
+    t_max, t_min = ts.loz_extremal(d)
+    p = loz_p_up_grid(d, ts.Uniform())
+    h = LozengeHandle(d, chains)
+    h.set_p_up(p)
+    h.upload(np.stack([t_min.edges] * chains))
+    seeds = np.arange(70, 70 + chains, dtype=np.uint64)
+    step = 60 * m * m
+    h.walk(seeds, step)
+    acc = np.zeros((3,) + t_min.edges.shape[1:])
+    for _ in range(8):
+        h.walk(seeds, 2 * m * m, step0=step)
+        step += 2 * m * m
+        acc += h.download().astype(np.float64).sum(axis=0)
+    dens = acc / (8 * chains)
+    X, Y = np.meshgrid(np.arange(dens.shape[1]) - m, np.arange(dens.shape[2]) - m, indexing="ij")
+    r = np.hypot(X + Y / 2.0, Y * np.sqrt(3.0) / 2.0)
+    inr = m * np.sqrt(3.0) / 2.0
+    vm = d.vertex_mask
+    out = vm & (r > 1.1 * inr)
+    frozen = np.minimum(dens, 1 - dens)[:, out]
+    assert frozen.max() < 0.05, frozen.max()
+    inner = dens[:, vm & (r < 0.5 * inr)]
+    assert np.all(np.abs(inner.mean(axis=1) - 1.0 / 3.0) < 0.05), inner.mean(axis=1)
