@@ -214,7 +214,7 @@ def c5full(torch, stream, quick):
     from paper_1804_07250_b200.sweeps import DominoHandle
     from paper_1804_07250_b200 import _native
 
-    order, count = (64, 4) if quick else (512, 8)
+    order, count = (64, 4) if quick else (512, int(os.environ.get("TSB_C5_COUNT", "8")))
     d = ts.Domain.aztec(order)
     t_max, t_min = aztec_extremal_states(order)
     h = DominoHandle(d, d.n + 1, 2 * count + 2)
