@@ -122,3 +122,129 @@ def aztec_y_intercept_from_density(grid: np.ndarray) -> float:
         else:
             break
     return float(boundary - mid)
+
+
+# -- host mirrors of the reference's statistics API (stats.py:28-315) ----------
+# Post-processing of host state objects, kept so that code written against
+# the reference's `tilesampler.stats` runs unchanged; the device path above
+# (DeviceDensity) computes the same density maps without downloading states.
+
+C_VERTEX_CODES = (0b1001, 0b0110)
+
+
+@dataclass(frozen=True)
+class ChiSquareResult:
+    statistic: float
+    dof: int
+    pvalue: float
+    significance: float
+
+    @property
+    def passed(self) -> bool:
+        return self.pvalue >= self.significance
+
+
+def chi_square_gof(counts, probs=None, significance: float = 0.001) -> ChiSquareResult:
+    """stats.py:40-60: chi-square goodness of fit (uniform when probs is None)."""
+    from scipy import stats as sps
+
+    counts = np.asarray(list(counts), dtype=float)
+    n = counts.sum()
+    if probs is None:
+        expected = np.full(len(counts), n / len(counts))
+    else:
+        probs = np.asarray(list(probs), dtype=float)
+        expected = probs / probs.sum() * n
+    stat = float(((counts - expected) ** 2 / expected).sum())
+    dof = len(counts) - 1
+    return ChiSquareResult(stat, dof, float(sps.chi2.sf(stat, dof)), significance)
+
+
+def total_variation(emp: dict, exact: dict) -> float:
+    """stats.py:63-65."""
+    keys = set(emp) | set(exact)
+    return 0.5 * sum(abs(emp.get(k, 0.0) - exact.get(k, 0.0)) for k in keys)
+
+
+def domino_orientation_grid(t) -> np.ndarray:
+    """stats.py:187-200: 1.0 where a face is covered by a horizontal domino
+    (its left or right edge is interior to a domino: tilestate bit 2 "down"
+    of its top corners), 0.0 for a vertical one, NaN outside the domain."""
+    s = np.asarray(t.states)
+    horiz = ((s[:-1, :-1] & 2) | (s[:-1, 1:] & 2)) != 0
+    return np.where(t.domain.faces, horiz.astype(float), np.nan)
+
+
+def _c_vertex_grid(state) -> np.ndarray:
+    from .sixvertex import vertex_type_codes
+
+    codes = vertex_type_codes(state)
+    return (codes == C_VERTEX_CODES[0]) | (codes == C_VERTEX_CODES[1])
+
+
+_OBSERVABLES = {
+    "h-edge": lambda st: st.h_edges.astype(float),
+    "v-edge": lambda st: st.v_edges.astype(float),
+    "c-vertex": lambda st: _c_vertex_grid(st).astype(float),
+    "domino-orientation": domino_orientation_grid,
+}
+
+
+def density_map(archive, observable: str) -> DensityMap:
+    """stats.py:231-245: per-site mean of the named indicator over an archive
+    of host states (for device-resident chains use DeviceDensity)."""
+    from .errors import EmptyArchive
+
+    if len(archive) == 0:
+        raise EmptyArchive("archive holds no records")
+    fn = _OBSERVABLES.get(observable)
+    if fn is None:
+        raise KeyError(f"unknown observable {observable!r}; have {sorted(_OBSERVABLES)}")
+    acc = None
+    for state in archive.records:
+        grid = fn(state)
+        acc = grid if acc is None else acc + grid
+    return DensityMap(observable, acc / len(archive), len(archive))
+
+
+@dataclass(frozen=True)
+class Histogram:
+    observable: str
+    edges: np.ndarray
+    density: np.ndarray
+    samples: int
+
+    def to_csv(self) -> str:
+        lines = ["left,right,density"]
+        for lo, hi, d in zip(self.edges[:-1], self.edges[1:], self.density):
+            lines.append(f"{lo:.6f},{hi:.6f},{d:.6f}")
+        return "\n".join(lines) + "\n"
+
+
+def c_vertex_count(state) -> float:
+    """stats.py:262-264."""
+    return float(_c_vertex_grid(state).sum())
+
+
+def aztec_y_intercept(t) -> float:
+    """stats.py:267-288."""
+    return aztec_y_intercept_from_density(domino_orientation_grid(t))
+
+
+def scalar_observable(archive, fn, bins=None) -> Histogram:
+    """stats.py:291-315: normalised histogram of a scalar observable
+    ('c-vertex-count', 'y-intercept' or a callable) over an archive."""
+    from .errors import EmptyArchive
+
+    if len(archive) == 0:
+        raise EmptyArchive("archive holds no records")
+    name = fn if isinstance(fn, str) else getattr(fn, "__name__", "scalar")
+    if fn == "c-vertex-count":
+        fn = c_vertex_count
+    elif fn == "y-intercept":
+        fn = aztec_y_intercept
+    values = np.array([fn(s) for s in archive.records], dtype=float)
+    lo, hi = values.min(), values.max()
+    edges = np.array([lo - 0.5, lo + 0.5]) if lo == hi else np.histogram_bin_edges(values, bins=bins or "auto")
+    density, edges = np.histogram(values, bins=edges, density=True)
+    return Histogram(name, edges, density, len(values))
