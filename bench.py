@@ -62,7 +62,7 @@ def parse():
                    help="N>1: independent chains per GPU (weak scaling) or one strip-sharded chain "
                         "(strong scaling); auto = strips above order 8192")
     p.add_argument("--replicas", action="store_true", help="alias for --mode replicas")
-    p.add_argument("--halo", type=int, default=32, help="strip sharding: halo rows = sweeps between exchanges")
+    p.add_argument("--halo", type=int, default=64, help="strip sharding: halo rows = sweeps between exchanges")
     p.add_argument("--host-exchange", action="store_true",
                    help="strip sharding: host-driven NCCL halo exchange instead of the device push/pull kernels")
     return p.parse_args()
@@ -84,7 +84,7 @@ def workload(order: int):
 
 
 MK = 2            # sweeps per domino_multi_kernel launch (kMK in csrc/domino.cu)
-GRAPH_SWEEPS = 32  # sweeps per CUDA-graph replay (kGraphSweeps)
+GRAPH_SWEEPS = 64  # sweeps per CUDA-graph replay (kGraphSweeps)
 
 
 def launches_per_walk(n: int) -> int:

@@ -48,7 +48,7 @@ struct tsb_domino {
     int (*g_tail)(tsb_domino *, cudaStream_t) = nullptr;
 };
 
-constexpr int kGraphSweeps = 32;
+constexpr int kGraphSweeps = 64;
 constexpr int kStatePad = 2;  // == kPad in domino.cu: zero words left of every state row
 
 

@@ -117,12 +117,12 @@ def _ipc_worker(rank, world, port, out_dir, halo, steps):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,halo", [(2, 32), (3, 32), (2, 16)])
+@pytest.mark.parametrize("world,halo", [(2, 64), (3, 32), (2, 16)])
 def test_device_strips_ipc_processes(tmp_path, world, halo):
     """The same exchange across processes through CUDA IPC handles (here all
-    processes share cuda:0; on the 8-GPU box each has its own GPU).  halo 32
-    runs the rounds as graph replays with the exchange captured as their
-    tail, halo 16 as explicit per-round launches."""
+    processes share cuda:0; on the 8-GPU box each has its own GPU).  halo 64
+    (= kGraphSweeps) runs the rounds as graph replays with the exchange
+    captured as their tail, halo 32 / 16 as explicit per-round launches."""
     import paper_1804_07250_b200 as ts
     from paper_1804_07250_b200.lattice import aztec_extremal_states
 
