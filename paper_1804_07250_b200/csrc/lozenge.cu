@@ -26,7 +26,7 @@
 namespace tsb {
 constexpr int kLzRows = 15;   // output rows per tile (+1 halo fire row)
 constexpr int kLzWords = 62;  // output words per tile
-constexpr int kLzGraph = 32;  // sweeps per CUDA graph
+constexpr int kLzGraph = 128;  // sweeps per CUDA graph
 constexpr int kLzMRows = 16;  // rows per temporally blocked tile (warps per block)
 constexpr size_t kLzMSmem = sizeof(uint4) * kLzMRows * 32 + sizeof(uint2) * kLzMRows * 32 +
                             sizeof(uint32_t) * kLzMRows * 64 + sizeof(uint16_t) * kLzMRows * 1024;

@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(256) sv_coalesced_kernel(const uint32_t *bits,
     if (threadIdx.x == 0) flags[j] = (any || h00[chain0 + 2 * j] != h00[chain0 + 2 * j + 1]) ? 0 : 1;
 }
 
-constexpr int kSvGraphSweeps = 32;  // sweeps per graph replay
+constexpr int kSvGraphSweeps = 128;  // sweeps per graph replay
 
 // Tile geometry of sv_multi_kernel: rows of W <= 128 words fit one column
 // tile (WPL = ceil(W/32) words per lane, no word halo); wider grids use
