@@ -225,3 +225,22 @@ def test_p_up_parity_matches_grid():
         assert (plan.p_up[par == 0] == pe).all() and (plan.p_up[par == 1] == po).all()
     assert ts.SweepPlan(d, ts.VolumeWeights(0.7, {(2, 3): 0.4})).p_up_parity is None
     assert ts.SweepPlan(d, ts.EdgeWeights(1.0, {((0, 0), (0, 1)): 2.0})).p_up_parity is None
+
+
+def test_c_abi_header_is_plain_c(tmp_path):
+    """include/tsb.h compiles as C99 and C++17 (the FFI boundary carries no
+    C++ or torch types) and a C program links against libtsb.so."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.c"
+    src.write_text('#include "include/tsb.h"\n#include <stdio.h>\n'
+                   'int main(void) { printf("%d\\n", tsb_abi_version()); return 0; }\n')
+    lib_dir = os.path.join(root, "paper_1804_07250_b200", "_lib")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", root, str(src), "-L", lib_dir, "-ltsb",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(tmp_path / "t")], check=True)
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", "-I", root, "-x", "c++", "-c", str(src), "-o",
+                    str(tmp_path / "t.o")], check=True)
+    out = subprocess.run([str(tmp_path / "t")], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "1"
