@@ -48,6 +48,8 @@ struct tsb_sv {
     uint32_t *bits2 = nullptr;  // second buffer (out-of-place launches)
     uint64_t *step_dev = nullptr;
     int m_wpl = 1, m_nw = 8, m_K = 4, m_out = 8, m_stride = 32, m_woff = 0, m_gx = 1, m_gy = 1;
+    bool m_k_fixed = false;  // TSB_SV_K given: no per-batch choice of K
+    int m_sms = 148;
     size_t m_smem = 0;
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
@@ -502,13 +504,28 @@ void sv_multi_config(tsb_sv *h) {
     }
     int nw = 16, K = 8;
     if (const char *e = getenv("TSB_SV_NW")) nw = atoi(e) == 16 ? 16 : 8;
-    if (const char *e = getenv("TSB_SV_K")) K = atoi(e);
+    if (const char *e = getenv("TSB_SV_K")) {
+        K = atoi(e);
+        h->m_k_fixed = true;
+    }
+    cudaDeviceGetAttribute(&h->m_sms, cudaDevAttrMultiProcessorCount, h->device);
     if (K != 2 && K != 4 && K != 8 && K != 16) K = 4;
     while (2 * nw - 2 * K < 2) K /= 2;
     h->m_nw = nw;
     h->m_K = K;
     h->m_out = 2 * nw - 2 * K;
     h->m_gy = (h->f + h->m_out - 1) / h->m_out;
+}
+
+// Sweeps per launch for a batch of n chains: a single lattice is latency
+// bound and takes K = 8 (fewer launches); once the batch fills two waves
+// with K = 4 tiles the halo redundancy dominates and K = 4 (24 of 32 rows
+// exact) is faster (DWBC 2048 x 32 chains: 0.20 -> 0.27 of the roofline).
+static int sv_k(const tsb_sv *h, int n) {
+    if (h->m_k_fixed || h->m_K != 8 || 2 * h->m_nw - 8 < 2) return h->m_K;
+    const int out4 = 2 * h->m_nw - 8;
+    const int64_t blocks = (int64_t)n * h->m_gx * ((h->f + out4 - 1) / out4);
+    return blocks >= 2 * (int64_t)h->m_sms ? 4 : 8;
 }
 
 template <int WPL, int NW>
@@ -536,14 +553,14 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
     c.f = h->f;
     c.W = h->W;
     c.pitch = h->pitch;
-    c.K = h->m_K;
-    c.out_rows = h->m_out;
+    c.K = sv_k(h, n);
+    c.out_rows = 2 * h->m_nw - 2 * c.K;
     c.stride = h->m_stride;
     c.woff = h->m_woff;
     c.step = step_off;
     for (int i = 0; i < 32; ++i) c.lut[i] = h->lut[i];
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(h->m_gx, h->m_gy, n);
+    cfg.gridDim = dim3(h->m_gx, (h->f + c.out_rows - 1) / c.out_rows, n);
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -575,9 +592,9 @@ static int sv_ensure_graph(tsb_sv *h, int chain0, int n) {
     cudaGraph_t g = nullptr;
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
-    const int launches = kSvGraphSweeps / h->m_K;
+    const int K = sv_k(h, n), launches = kSvGraphSweeps / K;
     for (int i = 0; i < launches && !rc; ++i)
-        rc = sv_launch_multi(h, chain0, n, (uint64_t)i * h->m_K, (i & 1) ? h->bits2 : h->bits,
+        rc = sv_launch_multi(h, chain0, n, (uint64_t)i * K, (i & 1) ? h->bits2 : h->bits,
                              (i & 1) ? h->bits : h->bits2, h->cap_stream);
     sv_advance_step<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kSvGraphSweeps);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -859,11 +876,12 @@ static int sv_walk_impl(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uin
         for (uint64_t r = 0; r < replays; ++r) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
         done = replays * kSvGraphSweeps;
     }
-    if (class_override < 0 && n_steps - done >= (uint64_t)h->m_K) {
+    const uint64_t Kn = (uint64_t)sv_k(h, n);
+    if (class_override < 0 && n_steps - done >= Kn) {
         // remainder: direct multi-sweep launches bits -> bits2 -> ..., step_dev = step0 + done
         if (done == 0) sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
         int launches = 0;
-        for (uint64_t i = 0; done + h->m_K <= n_steps; done += h->m_K, i += h->m_K, ++launches)
+        for (uint64_t i = 0; done + Kn <= n_steps; done += Kn, i += Kn, ++launches)
             if ((rc = sv_launch_multi(h, chain0, n, i, (launches & 1) ? h->bits2 : h->bits,
                                       (launches & 1) ? h->bits : h->bits2, h->stream)))
                 return rc;

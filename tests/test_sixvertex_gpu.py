@@ -137,3 +137,18 @@ def test_multi_k_nw(monkeypatch, K, NW, WPL, n):
     h.walk(seeds, 70)
     h.walk(seeds, steps - 70, step0=70)
     assert np.array_equal(h.download(), oracle.sv_walk(start, seeds, weights.table(), steps))
+
+
+def test_large_batch_uses_batch_geometry():
+    """40 chains: the per-batch sweeps-per-launch choice (K = 4 once the batch
+    fills two waves) is bit-identical to the oracle."""
+    n, steps, B = 300, 150, 40
+    hi, lo = closed_form(n)
+    start = np.stack([lo if k % 2 else hi for k in range(B)]).astype(np.int32)
+    seeds = np.arange(1000, 1000 + B, dtype=np.uint64)
+    w = ts.SVWeights(1.0, 1.0, 1.25)
+    h = SixVertexHandle(n, B)
+    h.set_weights(w)
+    h.upload(start)
+    h.walk(seeds, steps)
+    assert np.array_equal(h.download(), oracle.sv_walk(start, seeds, w.table(), steps))

@@ -204,6 +204,47 @@ def mixed(torch, stream, quick):
             "attempts_per_s": att / dt}
 
 
+def batched(torch, stream, quick):
+    """C2 and C3 lattices with 32 independent chains per launch (chains are
+    the multi-GPU replica unit): the single-chain configs are latency-bound,
+    the batch shows the kernels' throughput at the same lattice size."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lozenge import LozengeHandle, loz_p_up_grid
+    from paper_1804_07250_b200.sixvertex import SixVertexHandle
+
+    B = 8 if quick else 32
+    out = []
+    a = 300 if quick else 1000
+    d = ts.TriDomain.hexagon(a, a, a)
+    t_max, t_min = ts.loz_extremal(d)
+    h = LozengeHandle(d, B)
+    h.set_stream(stream.cuda_stream)
+    h.set_p_up(loz_p_up_grid(d, ts.VolumeWeights(0.999)))
+    h.upload(np.stack([t_min.edges] * B))
+    seeds = np.arange(1, B + 1, dtype=np.uint64)
+    h.walk(seeds, 256)
+    steps = 2048
+    dt = timed(torch, stream, lambda: h.walk(seeds, steps, step0=256))
+    nv = int(d.vertex_mask.sum())
+    att = B * nv / 3 * steps / dt
+    out.append({"config": f"C2 lattice x{B} chains: lozenge hexagon {a}^3 q=0.999 from T_min, {steps} sweeps",
+                "us_per_sweep_all_chains": dt / steps * 1e6, "attempts_per_s": att,
+                "roofline_frac": att * 2.25 / 1e9 / 6463.7})
+    n = 512 if quick else 2048
+    hi, lo = ts.sv_extremal(n, ts.dwbc(n))
+    h = SixVertexHandle(n, B)
+    h.set_stream(stream.cuda_stream)
+    h.set_weights(ts.SVWeights(1.0, 1.0, 1.0))
+    h.upload(np.stack([lo.heights] * B))
+    h.walk(seeds, 256)
+    dt = timed(torch, stream, lambda: h.walk(seeds, steps, step0=256))
+    att = B * (n - 1) ** 2 / 4 * steps / dt
+    out.append({"config": f"C3 lattice x{B} chains: six-vertex DWBC n={n} Delta=1/2 from h_min, {steps} sweeps",
+                "us_per_sweep_all_chains": dt / steps * 1e6, "attempts_per_s": att,
+                "roofline_frac": att * 2.0 / 1e9 / 6463.7})
+    return out
+
+
 def c5full(torch, stream, quick):
     """C5 to completion: exact CFTP samples of the Aztec diamond of order 512
     (cftp_sample_many, coupled T_max / T_min chains, doubling rounds) for a
