@@ -294,7 +294,20 @@ def make_archives():
     save("archives.npz", **arrays)
 
 
+def make_cli():
+    """Outputs of the reference CLI (cli.py:128-255) for gc.CLI_CASES, written
+    to cli_<name>.txt through its --out flag."""
+    from tilesampler.cli import main
+
+    for name, argv in gc.CLI_CASES:
+        out = os.path.join(HERE, f"cli_{name}.txt")
+        code = main([a.replace("{g}", HERE) for a in argv] + ["--out", out])
+        assert code == 0, (name, code)
+        print(f"cli {name}: {os.path.getsize(out)} B")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables", "archives"]
+    which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables", "archives",
+                             "cli"]
     for w in which:
         globals()[f"make_{w}"]()

@@ -196,3 +196,26 @@ class _LazyLoz(list):
 LOZ_CASES = _LazyLoz()
 LOZ_EXTREMAL = [(1, 1, 1), (2, 2, 2), (3, 4, 5), (6, 1, 3)]
 LOZ_CFTP_CASES = [((1, 1, 1), 5, 4), ((2, 2, 2), 77, 3)]
+
+# CLI runs (cli.py:128-255): name -> argv; "{g}" is the golden directory.
+# `density` / `hist` read the archives the `cftp` cases wrote.
+CLI_CASES = [
+    ("sample_domino_aztec", ["sample", "--model", "domino", "--aztec", "6", "--steps", "100", "--samples", "3",
+                             "--seed", "0x2a", "--weights", "q=0.9"]),
+    ("sample_domino_square", ["sample", "--square", "4", "--steps", "64", "--samples", "10"]),
+    ("sample_lozenge", ["sample", "--model", "lozenge", "--hexagon", "3,4,2", "--steps", "50", "--samples", "2",
+                        "--weights", "q=0.8", "--seed", "7"]),
+    ("sample_sixvertex", ["sample", "--model", "sixvertex", "--dwbc", "6", "--steps", "40", "--samples", "3",
+                          "--weights", "a=1,b=1,c=1.5", "--backend", "threads"]),
+    ("cftp_domino", ["cftp", "--aztec", "3", "--samples", "8", "--seed", "0x2a"]),
+    ("cftp_lozenge", ["cftp", "--model", "lozenge", "--hexagon", "2,2,2", "--samples", "4", "--seed", "5",
+                      "--weights", "q=1.2"]),
+    ("cftp_sixvertex", ["cftp", "--model", "sixvertex", "--dwbc", "4", "--samples", "5", "--seed", "9",
+                        "--weights", "a=1,b=1,c=2"]),
+    ("density_domino", ["density", "--aztec", "3", "--in", "{g}/cli_cftp_domino.txt",
+                        "--observable", "domino-orientation"]),
+    ("density_sixvertex_csv", ["density", "--model", "sixvertex", "--dwbc", "4", "--in", "{g}/cli_cftp_sixvertex.txt",
+                               "--observable", "c-vertex", "--format", "csv"]),
+    ("hist_sixvertex", ["hist", "--model", "sixvertex", "--dwbc", "4", "--in", "{g}/cli_cftp_sixvertex.txt"]),
+    ("hist_domino_y", ["hist", "--aztec", "3", "--in", "{g}/cli_cftp_domino.txt", "--observable", "y-intercept"]),
+]
