@@ -297,6 +297,131 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
     }
 }
 
+// Small lattices: one block per chain keeps the whole chain in shared memory
+// for all n_steps sweeps of a walk (one launch, no global traffic between
+// sweeps).  Thread t owns the (row, word) items t, t + blockDim, ...; per
+// sweep: fire words F (each warp deals the coins of its rotateable active
+// sites to its lanes), barrier, edge toggles in place, barrier.  The same
+// rotate/update semantics as the tiled kernels (_kernels.py:35-69); chosen
+// for tiny lattices and for batches of small lattices (CFTP) -- see
+// resident_smem for the rule.
+constexpr int kResThreads = 1024;
+constexpr int kResMaxItems = 512;
+constexpr int kResMinChains = 16;
+constexpr size_t kResScratch = (8 + 4 + 2 * 16) * 32 * 32;  // per-warp site bases, fire words, coin queues
+
+struct ResCtx {
+    uint2 *state;              // chain 0, row 0, word 0; updated in place
+    const uint64_t *seedinfo;  // [n][2]
+    const uint64_t *tgrid;
+    uint64_t t0, t1;
+    size_t chain_stride;
+    int side, pitch, W;
+    uint64_t step0, n_steps;
+};
+
+// Coins of a warp's rotateable active sites, dealt round-robin to its lanes
+// (two splitmix64 chains per lane per round, as warp_fire): lane l's word
+// starts at site sb and has rotateable bits ra (ia: the site is in state 3).
+template <int TM>
+__device__ __forceinline__ uint32_t res_coins(uint32_t ra, uint32_t ia, uint64_t sb, uint16_t *queue, uint32_t *fres,
+                                              uint64_t *sbase, uint64_t base, uint64_t salt, uint64_t t,
+                                              const uint64_t *__restrict__ tgrid) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = __popc(ra);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - cnt;
+    for (uint32_t m = ra; m; m &= m - 1) {  // job = is3 << 10 | lane << 5 | bit
+        const int b = __ffs(m) - 1;
+        queue[pos++] = (uint16_t)((((ia >> b) & 1u) << 10) | (lane << 5) | b);
+    }
+    fres[lane] = 0u;
+    sbase[lane] = sb;
+    __syncwarp();
+    for (int j = lane; j < total; j += 64) {
+        const bool two = j + 32 < total;
+        const uint32_t q0 = queue[j], q1 = two ? queue[j + 32] : q0;
+        const uint64_t s0 = sbase[(q0 >> 5) & 31u] + (q0 & 31u), s1 = sbase[(q1 >> 5) & 31u] + (q1 & 31u);
+        const uint64_t x0 = mix64(mix64(base + (s0 + 1ull) * kGold) + salt);
+        const uint64_t x1 = mix64(mix64(base + (s1 + 1ull) * kGold) + salt);
+        const uint64_t t0 = TM == 2 ? __ldg(tgrid + s0) : t;
+        const uint64_t t1 = TM == 2 ? __ldg(tgrid + s1) : t;
+        if (((x0 >> 11) < t0) == (bool)((q0 >> 10) & 1u)) atomicOr(&fres[(q0 >> 5) & 31u], 1u << (q0 & 31u));
+        if (two && ((x1 >> 11) < t1) == (bool)((q1 >> 10) & 1u)) atomicOr(&fres[(q1 >> 5) & 31u], 1u << (q1 & 31u));
+    }
+    __syncwarp();
+    const uint32_t f = fres[lane];
+    __syncwarp();  // fres / sbase / queue are reused by the warp's next item
+    return f;
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kResThreads, 1) domino_resident_kernel(ResCtx c) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int side = c.side, W = c.W, items = side * W;
+    const int warp = threadIdx.x >> 5;
+    uint64_t *sbase = reinterpret_cast<uint64_t *>(dsm) + 32 * warp;                         // [32 warps][32]
+    uint32_t *fres = reinterpret_cast<uint32_t *>(dsm + 8 * 32 * 32) + 32 * warp;              // [32][32]
+    uint16_t *queue = reinterpret_cast<uint16_t *>(dsm + 12 * 32 * 32) + 512 * warp;           // [32][512]
+    unsigned char *st = dsm + kResScratch;
+    uint2 *S = reinterpret_cast<uint2 *>(st);                                     // (side + 2) x W, guard rows
+    uint32_t *F = reinterpret_cast<uint32_t *>(st + sizeof(uint2) * (size_t)(side + 2) * W);  // (side + 1) x (W + 1)
+    const int z = blockIdx.x;
+    uint2 *g = c.state + (size_t)z * c.chain_stride;
+    for (int i = threadIdx.x; i < (side + 2) * W; i += blockDim.x) {
+        const int r = i / W - 1, w = i - (r + 1) * W;
+        S[i] = (r >= 0 && r < side) ? g[(ptrdiff_t)r * c.pitch + w] : make_uint2(0u, 0u);
+    }
+    for (int i = threadIdx.x; i < (side + 1) * (W + 1); i += blockDim.x) F[i] = 0u;
+    const uint64_t base = c.seedinfo[2 * z], gkey = c.seedinfo[2 * z + 1];
+    __syncthreads();
+#pragma unroll 1
+    for (uint64_t s = 0; s < c.n_steps; ++s) {
+        const uint64_t step = c.step0 + s;
+        const uint64_t salt = (step + 1ull) * kGold;
+        const int color = (int)(mix64(gkey + salt) >> 63);  // BLACK iff u < 1/2 (sweeps.py:266-269)
+        const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
+        for (int i0 = 0; i0 < items; i0 += blockDim.x) {  // warp-uniform trip count
+            const int i = i0 + threadIdx.x;
+            const int r = i / W, w = i - r * W;
+            uint32_t ra = 0u, ia = 0u;
+            if (i < items) {
+                const uint2 cur = S[i + W];
+                const uint32_t vu = S[i].x;
+                const uint32_t hp = w > 0 ? S[i + W - 1].y : 0u;
+                const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;
+                const uint32_t la = (cur.y << 1) | (hp >> 31);
+                ia = vu & cur.x & ~(la | cur.y);
+                ra = (ia | (~(vu | cur.x) & la & cur.y)) & (color ? ~act0 : act0);
+            }
+            uint32_t f = 0u;
+            if (__any_sync(0xffffffffu, ra != 0u))
+                f = res_coins<TM>(ra, ia, (uint64_t)r * (uint64_t)side + 32ull * (uint64_t)w, queue, fres, sbase,
+                                  base, salt, t, c.tgrid);
+            if (i < items) F[r * (W + 1) + w] = f;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int r = i / W, w = i - r * W;
+            const uint32_t *fr = F + r * (W + 1) + w;
+            const uint32_t f = fr[0], fn = fr[W + 1], fx = fr[1];
+            const uint2 cur = S[i + W];
+            S[i + W] = make_uint2(cur.x ^ f ^ fn, cur.y ^ f ^ (f >> 1) ^ (fx << 31));
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+        const int r = i / W, w = i - r * W;
+        g[(ptrdiff_t)r * c.pitch + w] = S[i + W];
+    }
+}
+
 // CFTP's coupled pairs (cftp.py:115-119): chains 2z and 2z+1 run from T_max /
 // T_min with the SAME seeds, so every coin is shared.  One block sweeps the
 // tile in both chains and draws each coin once, for the union of the two
@@ -937,10 +1062,58 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
 // device: graph replays, direct multi-sweep launches, single sweeps; the
 // walked chains end in the handle's canonical buffer.  Stream-ordered, no
 // host synchronisation.
+// Shared-memory bytes of a resident walk, 0 when the lattice is not eligible.
+// Default: tiny lattices (<= kResMaxItems words: a tiled launch is a few
+// blocks of pure latency) or batches of >= kResMinChains chains (the tiled
+// launches then queue many waves of small tiles while one resident block per
+// chain stays within about one wave; Aztec 128 x 128 chains: 8.2 -> 3.2 us
+// per sweep, Aztec 256: 13.4 -> 6.8).  A single chain of a larger lattice
+// keeps the tiled kernels (Aztec 128: 1.85 vs 3.1 us).
+static size_t resident_smem(const tsb_domino *h, int n) {
+    const char *ev = getenv("TSB_DOM_RESIDENT");  // 0: never, 1: whenever it fits (read per walk)
+    const int mode = ev ? atoi(ev) : -1;
+    if (mode == 0 || h->strip || h->win_mn != h->nmtiles || h->win_tn != h->ntiles) return 0;
+    const size_t items = (size_t)h->side * h->W;
+    if (mode < 0 && items > (size_t)kResMaxItems && n < kResMinChains) return 0;
+    const size_t bytes = kResScratch + sizeof(uint2) * (size_t)(h->side + 2) * h->W +
+                         sizeof(uint32_t) * (size_t)(h->side + 1) * (h->W + 1);
+    return bytes <= 200u * 1024u ? bytes : 0;
+}
+
+static int launch_resident(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps, size_t smem) {
+    ResCtx c;
+    c.state = h->buf[h->cur] + (size_t)chain0 * h->chain_stride + h->pitch + kPad;
+    c.seedinfo = h->seedinfo;
+    c.tgrid = h->tgrid;
+    c.t0 = h->t0;
+    c.t1 = h->t1;
+    c.chain_stride = h->chain_stride;
+    c.side = h->side;
+    c.pitch = h->pitch;
+    c.W = h->W;
+    c.step0 = step0;
+    c.n_steps = n_steps;
+    const size_t items = (size_t)h->side * h->W;
+    const int threads = (int)std::min<size_t>(kResThreads, (items + 31) / 32 * 32);
+    const void *fn = h->tmode == 0 ? (const void *)domino_resident_kernel<0>
+                   : h->tmode == 1 ? (const void *)domino_resident_kernel<1> : (const void *)domino_resident_kernel<2>;
+    TSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    switch (h->tmode) {
+        case 0: domino_resident_kernel<0><<<n, threads, smem, h->stream>>>(c); break;
+        case 1: domino_resident_kernel<1><<<n, threads, smem, h->stream>>>(c); break;
+        default: domino_resident_kernel<2><<<n, threads, smem, h->stream>>>(c); break;
+    }
+    TSB_CUDA(cudaGetLastError());
+    return TSB_OK;
+}
+
 int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps) {
     int rc;
     const int cur0 = h->cur;
     uint64_t s = 0;
+    if (n_steps >= 2) {
+        if (const size_t smem = resident_smem(h, n)) return launch_resident(h, chain0, n, step0, n_steps, smem);
+    }
     if (n_steps >= kGraphSweeps) {
         if ((rc = ensure_graph(h, chain0, n))) return rc;
         set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);

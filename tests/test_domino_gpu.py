@@ -298,6 +298,7 @@ def test_golden_walks_both_tile_widths(monkeypatch, wpl):
     """Every golden walk case with the multi-sweep tiles forced to 1 and to 2
     words per lane (the library picks per lattice; both must be exact)."""
     monkeypatch.setenv("TSB_DOM_WPL", str(wpl))
+    monkeypatch.setenv("TSB_DOM_RESIDENT", "0")  # the tiled kernels, even for the small cases
     g = np.load(os.path.join(G, "domino_walks.npz"))
     i = 0
     while f"c{i}_faces" in g:
@@ -319,3 +320,22 @@ def test_golden_walks_both_tile_widths(monkeypatch, wpl):
         h.upload(start)
         h.walk([5, 6], steps)
         assert np.array_equal(h.download(), oracle.domino_walk(start, [5, 6], plan.p_up, steps)), (order, wpl)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_resident_and_tiled_paths(monkeypatch, mode):
+    """The shared-memory resident walk (one block per chain for the whole
+    walk) and the tiled graph/multi-sweep kernels, each forced on every
+    golden walk case, the C1 fingerprint and the CFTP goldens (weights of all
+    three threshold modes: uniform, parity, per-site grid)."""
+    monkeypatch.setenv("TSB_DOM_RESIDENT", mode)
+    test_golden_walk_cases()
+    test_c1_fingerprint()
+    test_cftp_golden()
+    d = ts.Domain.aztec(40)
+    plan = ts.SweepPlan(d, ts.VolumeWeights(0.7))
+    t_max, t_min = ts.extremal_tilings(d)
+    start = np.stack([t_max.states, t_min.states] * 10)
+    seeds = np.arange(1, 21, dtype=np.uint64)
+    out = ts.random_walk_batch(start, seeds, 301, plan)
+    assert np.array_equal(out, oracle.domino_walk(start, seeds, plan.p_up, 301))
