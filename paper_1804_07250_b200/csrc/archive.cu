@@ -83,14 +83,14 @@ int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t
     const int side = h->side;
     const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride + kStatePad;
     unsigned long long *d_len = nullptr;
-    TSB_CUDA(cudaMalloc(&d_len, sizeof(unsigned long long) * side));
+    TSB_CUDA(cudaMallocAsync(&d_len, sizeof(unsigned long long) * side, h->stream));  // stream-ordered: no device sync
     dser_count_kernel<<<side, kSerThreads, 0, h->stream>>>(st, side, h->pitch, d_len);
     std::vector<unsigned long long> rl(side);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(rl.data(), d_len, sizeof(unsigned long long) * side, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
-        cudaFree(d_len);
+        cudaFreeAsync(d_len, h->stream);
         return cuda_fail(e, "serialize count");
     }
     unsigned long long acc = 0;
@@ -102,11 +102,11 @@ int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t
     const unsigned long long total = acc - 1;  // no separator after the last vertex
     *len = (size_t)total;
     if (!out || cap < total) {
-        cudaFree(d_len);
+        cudaFreeAsync(d_len, h->stream);
         return TSB_OK;  // size query
     }
     char *d_out = nullptr;
-    e = cudaMalloc(&d_out, acc);
+    e = cudaMallocAsync(&d_out, acc, h->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, rl.data(), sizeof(unsigned long long) * side, cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) {
         dser_write_kernel<<<side, kSerThreads, 0, h->stream>>>(st, side, h->pitch, d_len, total, d_out);
@@ -114,8 +114,8 @@ int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(d_out);
-    cudaFree(d_len);
+    if (d_out) cudaFreeAsync(d_out, h->stream);
+    cudaFreeAsync(d_len, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "serialize");
     return TSB_OK;
 }

@@ -1074,13 +1074,13 @@ int tsb_loz_serialize(tsb_loz *h, int chain, char *out, size_t cap, size_t *len)
     if (!out || cap < total) return TSB_OK;  // size query
     TSB_CUDA(cudaSetDevice(h->device));
     char *d = nullptr;
-    TSB_CUDA(cudaMalloc(&d, total));
+    TSB_CUDA(cudaMallocAsync(&d, total, h->stream));
     lz_serialize_kernel<<<dim3((h->W + 63) / 64, h->X, 3), 64, 0, h->stream>>>(
         h->buf[h->cur] + (size_t)chain * h->chain_words, h->X, h->Y, h->pitch, h->plane, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loz serialize");
     return TSB_OK;
 }
@@ -1090,13 +1090,13 @@ int tsb_loz_coalesced(tsb_loz *h, int chain0, int npairs, uint8_t *flags) {
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
     uint8_t *d = nullptr;
-    TSB_CUDA(cudaMalloc(&d, npairs));
+    TSB_CUDA(cudaMallocAsync(&d, npairs, h->stream));
     lz_coalesced<<<npairs, 256, 0, h->stream>>>(reinterpret_cast<const uint4 *>(h->buf[h->cur]), h->chain_words / 4,
                                                chain0, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, npairs, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loz coalesced");
     return TSB_OK;
 }

@@ -1003,14 +1003,14 @@ int tsb_sv_serialize(tsb_sv *h, int chain, char *out, size_t cap, size_t *len) {
     TSB_CUDA(cudaMemcpyAsync(&p00, h->h00 + chain, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     TSB_CUDA(cudaStreamSynchronize(h->stream));
     char *d = nullptr;
-    TSB_CUDA(cudaMalloc(&d, total));
+    TSB_CUDA(cudaMallocAsync(&d, total, h->stream));
     const int W = (h->n + 1 + 31) / 32;
     sv_serialize_kernel<<<dim3((W + 63) / 64, h->n + 1, 2), 64, 0, h->stream>>>(
         h->bits + (size_t)chain * h->chain_words, p00 & 1, h->pitch, h->n, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "sv serialize");
     return TSB_OK;
 }
@@ -1020,12 +1020,12 @@ int tsb_sv_coalesced(tsb_sv *h, int chain0, int npairs, uint8_t *flags) {
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
     uint8_t *d = nullptr;
-    TSB_CUDA(cudaMalloc(&d, npairs));
+    TSB_CUDA(cudaMallocAsync(&d, npairs, h->stream));
     sv_coalesced_kernel<<<npairs, 256, 0, h->stream>>>(h->bits, h->h00, h->chain_words, chain0, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, npairs, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(d);
+    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "sv coalesced");
     return TSB_OK;
 }
