@@ -38,6 +38,7 @@ constexpr int kPad = 2;         // zero words left of every state row (lane 0's 
 constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
+constexpr int kTpcMinTiles = 12288;     // launches of at least this many tiles pair them per block
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
@@ -166,30 +167,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TT(ph)
 #endif
 
+// kMK sweeps of one tile held in registers (cur) and shared memory, then the
+// exact central rows are stored.
 template <int TM>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
-    TT(0);
-    extern __shared__ __align__(16) unsigned char dsm[];
-    uint2(*vs)[32] = reinterpret_cast<uint2(*)[32]>(dsm);
-    uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
-    uint32_t(*fres)[64] = reinterpret_cast<uint32_t(*)[64]>(dsm + 2 * sizeof(uint2) * kMRows * 32);
-    uint16_t(*queue)[1024] =
-        reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64);
-    const int lane = threadIdx.x & 31;
-    const int k = threadIdx.x >> 5;
-    const int2 tile = c.tiles[blockIdx.x];
-    const int r = tile.y * kMOut - kMK + k;
-    const int wa = tile.x + 2 * lane;  // band-aligned tile: tile.x = first loaded word (even)
-    const int z = blockIdx.z;
-    const bool in_grid = r >= 0 && r < c.side;
-    const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    TT(1);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    TT(2);
-    uint4 cur = make_uint4(0u, 0u, 0u, 0u);
-    if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
-    const uint64_t step0 = *c.step_dev + c.step;
+__device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], uint2 (*fs)[32], uint32_t (*fres)[64],
+                                           uint16_t (*queue)[1024], int k, int lane, int z, int r, int wa,
+                                           bool in_grid, uint4 cur, uint64_t step0) {
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
@@ -239,7 +222,62 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
         else if (lane == 0) out[wa + 1] = make_uint2(cur.z, cur.w);
         else out[wa] = make_uint2(cur.x, cur.y);
     }
+}
+
+#define MULTI_SMEM                                                                                          \
+    extern __shared__ __align__(16) unsigned char dsm[];                                                    \
+    uint2(*vs)[32] = reinterpret_cast<uint2(*)[32]>(dsm);                                                   \
+    uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);                     \
+    uint32_t(*fres)[64] = reinterpret_cast<uint32_t(*)[64]>(dsm + 2 * sizeof(uint2) * kMRows * 32);         \
+    uint16_t(*queue)[1024] =                                                                                \
+        reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64)
+
+template <int TM>
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
+    TT(0);
+    MULTI_SMEM;
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int2 tile = c.tiles[blockIdx.x];
+    const int r = tile.y * kMOut - kMK + k;
+    const int wa = tile.x + 2 * lane;  // band-aligned tile: tile.x = first loaded word (even)
+    const int z = blockIdx.z;
+    const bool in_grid = r >= 0 && r < c.side;
+    const uint2 *row = c.src + (size_t)z * c.chain_stride + (ptrdiff_t)r * c.pitch;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    TT(1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    TT(2);
+    uint4 cur = make_uint4(0u, 0u, 0u, 0u);
+    if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
+    multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur, *c.step_dev + c.step);
     TT(5);
+}
+
+// Two tiles per block (HBM-streaming launches, see launch_multi): the second
+// tile's rows are loaded together with the first's, so their latency hides
+// behind the first tile's sweeps.
+template <int TM>
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi2t_kernel(SweepCtx c) {
+    MULTI_SMEM;
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
+    const int z = blockIdx.z;
+    const int i0 = 2 * blockIdx.x;
+    const bool has1 = i0 + 1 < c.ntiles;
+    const int2 ta = c.tiles[i0], tb = c.tiles[has1 ? i0 + 1 : i0];
+    const int ra = ta.y * kMOut - kMK + k, rb = tb.y * kMOut - kMK + k;
+    const int wa0 = ta.x + 2 * lane, wb0 = tb.x + 2 * lane;
+    const bool ga = ra >= 0 && ra < c.side, gb = has1 && rb >= 0 && rb < c.side;
+    const uint2 *base = c.src + (size_t)z * c.chain_stride;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint4 cura = make_uint4(0u, 0u, 0u, 0u), curb = cura;
+    if (ga) cura = __ldg(reinterpret_cast<const uint4 *>(base + (ptrdiff_t)ra * c.pitch + wa0));
+    if (gb) curb = __ldg(reinterpret_cast<const uint4 *>(base + (ptrdiff_t)rb * c.pitch + wb0));
+    const uint64_t step0 = *c.step_dev + c.step;
+    multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, ra, wa0, ga, cura, step0);
+    if (has1) multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, rb, wb0, gb, curb, step0);
 }
 
 // The same temporal blocking with ONE {V,H} word per lane (tiles of 30 output
@@ -713,6 +751,21 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
         }
         return TSB_OK;
     }
+    // Two tiles per block once a launch streams more tiles than L2 holds
+    // (>= kTpcMinTiles x 8 KB loaded): the prefetched second tile keeps more
+    // loads in flight (Aztec 12288: 36.0 -> 31.2 us per sweep, 16384: 61.7 ->
+    // 53.4).  L2-resident launches keep one tile per block: pairing doubles
+    // the block of the slowest, RNG-heavy tiles (Aztec 4096: 6.0 -> 10.2 us).
+    const bool two = h->m_tpc == 2 || (h->m_tpc == 0 && (size_t)h->win_mn * (size_t)n >= (size_t)kTpcMinTiles);
+    if (two) {
+        cfg.gridDim.x = (h->win_mn + 1) / 2;
+        switch (h->tmode) {
+            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<0>, c)); break;
+            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<1>, c)); break;
+            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<2>, c)); break;
+        }
+        return TSB_OK;
+    }
     switch (h->tmode) {
         case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<0>, c)); break;
         case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<1>, c)); break;
@@ -907,6 +960,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         int wpl = (size_t)t1.size() * 32 < mtiles.size() * 64 * 9 / 10 ? 1 : 2;  // 1 only when clearly cheaper
         if (const char *ev = getenv("TSB_DOM_WPL")) wpl = atoi(ev) == 1 ? 1 : 2;
         h->m_wpl = wpl;
+        if (const char *ev = getenv("TSB_DOM_TPC")) h->m_tpc = atoi(ev) == 2 ? 2 : 1;  // force; default auto
         if (wpl == 1) {
             mtiles.swap(t1);
             h->mband_start.swap(b1);
@@ -926,7 +980,8 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         (e = cudaMemcpy(h->mtiles, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
         return bail(e, "mtiles");
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
-                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
+                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi2t_kernel<0>,
+                           (const void *)domino_multi2t_kernel<1>, (const void *)domino_multi2t_kernel<2>, (const void *)domino_multi1_kernel<0>,
                            (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>,
                            (const void *)domino_multi1c_kernel<0>, (const void *)domino_multi1c_kernel<1>,
                            (const void *)domino_multi1c_kernel<2>})
