@@ -82,17 +82,17 @@ int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t
     TSB_CUDA(cudaSetDevice(h->device));
     const int side = h->side;
     const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride + kStatePad;
-    unsigned long long *d_len = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d_len, sizeof(unsigned long long) * side, h->stream));  // stream-ordered: no device sync
+    // scratch: the handle's staging buffer (row lengths, then offsets + text)
+    const size_t len_bytes = sizeof(unsigned long long) * (size_t)side;
+    int rc = ensure_bytes(h, len_bytes);
+    if (rc) return rc;
+    unsigned long long *d_len = reinterpret_cast<unsigned long long *>(h->bytes);
     dser_count_kernel<<<side, kSerThreads, 0, h->stream>>>(st, side, h->pitch, d_len);
     std::vector<unsigned long long> rl(side);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(rl.data(), d_len, sizeof(unsigned long long) * side, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(rl.data(), d_len, len_bytes, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (e != cudaSuccess) {
-        cudaFreeAsync(d_len, h->stream);
-        return cuda_fail(e, "serialize count");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "serialize count");
     unsigned long long acc = 0;
     for (int r = 0; r < side; ++r) {
         const unsigned long long l = rl[r];
@@ -101,21 +101,17 @@ int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t
     }
     const unsigned long long total = acc - 1;  // no separator after the last vertex
     *len = (size_t)total;
-    if (!out || cap < total) {
-        cudaFreeAsync(d_len, h->stream);
-        return TSB_OK;  // size query
-    }
-    char *d_out = nullptr;
-    e = cudaMallocAsync(&d_out, acc, h->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, rl.data(), sizeof(unsigned long long) * side, cudaMemcpyHostToDevice, h->stream);
+    if (!out || cap < total) return TSB_OK;  // size query
+    if ((rc = ensure_bytes(h, len_bytes + acc))) return rc;
+    d_len = reinterpret_cast<unsigned long long *>(h->bytes);
+    char *d_out = reinterpret_cast<char *>(h->bytes) + len_bytes;
+    e = cudaMemcpyAsync(d_len, rl.data(), len_bytes, cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) {
         dser_write_kernel<<<side, kSerThreads, 0, h->stream>>>(st, side, h->pitch, d_len, total, d_out);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (d_out) cudaFreeAsync(d_out, h->stream);
-    cudaFreeAsync(d_len, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "serialize");
     return TSB_OK;
 }

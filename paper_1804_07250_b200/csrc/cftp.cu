@@ -55,15 +55,14 @@ int tsb_domino_coalesced(tsb_domino *h, int chain0, int npairs, uint8_t *flags) 
     int rc = check_range(h, chain0, 2 * npairs);
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
-    uint8_t *d = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d, npairs, h->stream));  // stream-ordered: no device-wide sync
+    if ((rc = ensure_bytes(h, npairs))) return rc;  // handle scratch: no allocation per round
+    uint8_t *d = h->bytes;
     const size_t chain_u4 = h->chain_stride / 2;  // chain_stride is even (pitch % 32 == 0)
     coalesced_kernel<<<npairs, 256, 0, h->stream>>>(reinterpret_cast<const uint4 *>(h->buf[h->cur]),
                                                    chain_u4, chain0, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, npairs, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "coalesced");
     return TSB_OK;
 }

@@ -1073,14 +1073,13 @@ int tsb_loz_serialize(tsb_loz *h, int chain, char *out, size_t cap, size_t *len)
     *len = total;
     if (!out || cap < total) return TSB_OK;  // size query
     TSB_CUDA(cudaSetDevice(h->device));
-    char *d = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d, total, h->stream));
+    if ((rc = lz_bytes(h, total))) return rc;  // handle scratch: no allocation per record
+    char *d = reinterpret_cast<char *>(h->bytes);
     lz_serialize_kernel<<<dim3((h->W + 63) / 64, h->X, 3), 64, 0, h->stream>>>(
         h->buf[h->cur] + (size_t)chain * h->chain_words, h->X, h->Y, h->pitch, h->plane, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loz serialize");
     return TSB_OK;
 }
@@ -1089,14 +1088,13 @@ int tsb_loz_coalesced(tsb_loz *h, int chain0, int npairs, uint8_t *flags) {
     int rc = lz_check(h, chain0, 2 * npairs);
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
-    uint8_t *d = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d, npairs, h->stream));
+    if ((rc = lz_bytes(h, npairs))) return rc;
+    uint8_t *d = reinterpret_cast<uint8_t *>(h->bytes);
     lz_coalesced<<<npairs, 256, 0, h->stream>>>(reinterpret_cast<const uint4 *>(h->buf[h->cur]), h->chain_words / 4,
                                                chain0, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, npairs, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loz coalesced");
     return TSB_OK;
 }

@@ -1002,15 +1002,14 @@ int tsb_sv_serialize(tsb_sv *h, int chain, char *out, size_t cap, size_t *len) {
     int32_t p00 = 0;
     TSB_CUDA(cudaMemcpyAsync(&p00, h->h00 + chain, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     TSB_CUDA(cudaStreamSynchronize(h->stream));
-    char *d = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d, total, h->stream));
+    if ((rc = sv_hbuf(h, 1))) return rc;  // handle scratch (f^2 int32 >= total bytes): no allocation per record
+    char *d = reinterpret_cast<char *>(h->hbuf);
     const int W = (h->n + 1 + 31) / 32;
     sv_serialize_kernel<<<dim3((W + 63) / 64, h->n + 1, 2), 64, 0, h->stream>>>(
         h->bits + (size_t)chain * h->chain_words, p00 & 1, h->pitch, h->n, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, total, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "sv serialize");
     return TSB_OK;
 }
@@ -1019,13 +1018,12 @@ int tsb_sv_coalesced(tsb_sv *h, int chain0, int npairs, uint8_t *flags) {
     int rc = sv_check(h, chain0, 2 * npairs);
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
-    uint8_t *d = nullptr;
-    TSB_CUDA(cudaMallocAsync(&d, npairs, h->stream));
+    if ((rc = sv_hbuf(h, ((size_t)npairs + 4 * (size_t)h->f * h->f - 1) / (4 * (size_t)h->f * h->f)))) return rc;
+    uint8_t *d = reinterpret_cast<uint8_t *>(h->hbuf);
     sv_coalesced_kernel<<<npairs, 256, 0, h->stream>>>(h->bits, h->h00, h->chain_words, chain0, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, npairs, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFreeAsync(d, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "sv coalesced");
     return TSB_OK;
 }
