@@ -38,7 +38,7 @@ constexpr int kPad = 2;         // zero words left of every state row (lane 0's 
 constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
-constexpr int kTpcMinTiles = 12288;     // launches of at least this many tiles pair them per block
+constexpr int kPipeMinTiles = 12288;    // launches of at least this many tiles use the pipelined kernel
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
@@ -254,30 +254,53 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     TT(5);
 }
 
-// Two tiles per block (HBM-streaming launches, see launch_multi): the second
-// tile's rows are loaded together with the first's, so their latency hides
-// behind the first tile's sweeps.
+// Streaming launches, pipelined: persistent blocks (3 per SM) walk the tile
+// list with a grid stride; each thread's 16-byte slice of its NEXT tile is
+// fetched with cp.async into the thread's own shared-memory slot (double
+// buffered) while the current tile is swept, so the HBM latency of a tile
+// overlaps the sweeps of the previous one.  A thread only ever reads the slot
+// it filled itself, so cp.async.wait_group needs no block barrier.
+constexpr size_t kPipeSmem = kMSmem + 2 * sizeof(uint4) * 32 * kMRows;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
 template <int TM>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi2t_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(SweepCtx c) {
     MULTI_SMEM;
+    uint4 *slot = reinterpret_cast<uint4 *>(dsm + kMSmem) + threadIdx.x;  // [2][blockDim]
     const int lane = threadIdx.x & 31;
     const int k = threadIdx.x >> 5;
     const int z = blockIdx.z;
-    const int i0 = 2 * blockIdx.x;
-    const bool has1 = i0 + 1 < c.ntiles;
-    const int2 ta = c.tiles[i0], tb = c.tiles[has1 ? i0 + 1 : i0];
-    const int ra = ta.y * kMOut - kMK + k, rb = tb.y * kMOut - kMK + k;
-    const int wa0 = ta.x + 2 * lane, wb0 = tb.x + 2 * lane;
-    const bool ga = ra >= 0 && ra < c.side, gb = has1 && rb >= 0 && rb < c.side;
     const uint2 *base = c.src + (size_t)z * c.chain_stride;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    uint4 cura = make_uint4(0u, 0u, 0u, 0u), curb = cura;
-    if (ga) cura = __ldg(reinterpret_cast<const uint4 *>(base + (ptrdiff_t)ra * c.pitch + wa0));
-    if (gb) curb = __ldg(reinterpret_cast<const uint4 *>(base + (ptrdiff_t)rb * c.pitch + wb0));
     const uint64_t step0 = *c.step_dev + c.step;
-    multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, ra, wa0, ga, cura, step0);
-    if (has1) multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, rb, wb0, gb, curb, step0);
+    auto fetch = [&](int i, int b) {
+        const int2 t = c.tiles[i];
+        const int r = t.y * kMOut - kMK + k;
+        uint4 *dst = slot + b * 32 * kMRows;
+        if (r >= 0 && r < c.side) cp_async16(dst, base + (ptrdiff_t)r * c.pitch + t.x + 2 * lane);
+        else *dst = make_uint4(0u, 0u, 0u, 0u);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int b = 0;
+    if ((int)blockIdx.x < c.ntiles) fetch(blockIdx.x, 0);
+    for (int i = blockIdx.x; i < c.ntiles; i += gridDim.x, b ^= 1) {
+        const int nx = i + gridDim.x;
+        if (nx < c.ntiles) {
+            fetch(nx, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's group has landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const uint4 cur = slot[b * 32 * kMRows];
+        const int2 t = c.tiles[i];
+        const int r = t.y * kMOut - kMK + k;
+        multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
+    }
 }
 
 // The same temporal blocking with ONE {V,H} word per lane (tiles of 30 output
@@ -751,18 +774,19 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
         }
         return TSB_OK;
     }
-    // Two tiles per block once a launch streams more tiles than L2 holds
-    // (>= kTpcMinTiles x 8 KB loaded): the prefetched second tile keeps more
-    // loads in flight (Aztec 12288: 36.0 -> 31.2 us per sweep, 16384: 61.7 ->
-    // 53.4).  L2-resident launches keep one tile per block: pairing doubles
-    // the block of the slowest, RNG-heavy tiles (Aztec 4096: 6.0 -> 10.2 us).
-    const bool two = h->m_tpc == 2 || (h->m_tpc == 0 && (size_t)h->win_mn * (size_t)n >= (size_t)kTpcMinTiles);
-    if (two) {
-        cfg.gridDim.x = (h->win_mn + 1) / 2;
+    // Launches that stream more tiles than L2 holds (>= kPipeMinTiles x 8 KB
+    // loaded) use the persistent cp.async-pipelined kernel: Aztec 12288 36.0
+    // -> 29.1 us per sweep, C4 (Aztec 16384) 61.7 -> 51.3.  L2-resident
+    // launches keep one short-lived block per tile (pipelining Aztec 4096:
+    // 6.1 -> 7.1 us; its time is set by the slowest RNG-heavy tiles).
+    const bool big = (size_t)h->win_mn * (size_t)n >= (size_t)kPipeMinTiles;
+    if (h->m_pipe == 1 || (h->m_pipe < 0 && big)) {
+        cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
+        cfg.dynamicSmemBytes = kPipeSmem;
         switch (h->tmode) {
-            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<0>, c)); break;
-            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<1>, c)); break;
-            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi2t_kernel<2>, c)); break;
+            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<0>, c)); break;
+            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<1>, c)); break;
+            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<2>, c)); break;
         }
         return TSB_OK;
     }
@@ -960,7 +984,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         int wpl = (size_t)t1.size() * 32 < mtiles.size() * 64 * 9 / 10 ? 1 : 2;  // 1 only when clearly cheaper
         if (const char *ev = getenv("TSB_DOM_WPL")) wpl = atoi(ev) == 1 ? 1 : 2;
         h->m_wpl = wpl;
-        if (const char *ev = getenv("TSB_DOM_TPC")) h->m_tpc = atoi(ev) == 2 ? 2 : 1;  // force; default auto
+        if (const char *ev = getenv("TSB_DOM_PIPE")) h->m_pipe = atoi(ev) ? 1 : 0;  // force the pipelined kernel on / off
         if (wpl == 1) {
             mtiles.swap(t1);
             h->mband_start.swap(b1);
@@ -980,13 +1004,17 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         (e = cudaMemcpy(h->mtiles, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
         return bail(e, "mtiles");
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
-                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi2t_kernel<0>,
-                           (const void *)domino_multi2t_kernel<1>, (const void *)domino_multi2t_kernel<2>, (const void *)domino_multi1_kernel<0>,
+                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
                            (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>,
                            (const void *)domino_multi1c_kernel<0>, (const void *)domino_multi1c_kernel<1>,
                            (const void *)domino_multi1c_kernel<2>})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem)) != cudaSuccess)
             return bail(e, "smem attribute");
+    for (const void *fn : {(const void *)domino_multi_pipe_kernel<0>, (const void *)domino_multi_pipe_kernel<1>,
+                           (const void *)domino_multi_pipe_kernel<2>})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem)) != cudaSuccess)
+            return bail(e, "smem attribute");
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
         return bail(e, "cudaMalloc tiles");
     if (!tiles.empty() &&

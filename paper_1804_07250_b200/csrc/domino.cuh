@@ -21,7 +21,8 @@ struct tsb_domino {
     int nmtiles = 0;
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
-    int m_tpc = 0;  // tiles per block of the 2-word multi-sweep kernel: 0 auto, 1, 2 (TSB_DOM_TPC)
+    int m_pipe = -1;  // 2-word multi-sweep kernel: -1 auto, 0 one block per tile, 1 persistent pipelined (TSB_DOM_PIPE)
+    int num_sms = 148;
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
     bool coupled = false, g_coupled = false;  // chains 2j, 2j+1 share seeds (CFTP pairs): share the coins
     int tmode = 0;

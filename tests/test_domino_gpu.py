@@ -293,13 +293,14 @@ def test_c4_size_walk_windows_vs_oracle():
         assert np.array_equal(rows[a - lo:b - lo], out[a:b]), (a, b)
 
 
-@pytest.mark.parametrize("wpl,tpc", [(1, 1), (2, 1), (2, 2)])
-def test_golden_walks_both_tile_widths(monkeypatch, wpl, tpc):
+@pytest.mark.parametrize("wpl,pipe", [(1, 0), (2, 0), (2, 1)])
+def test_golden_walks_both_tile_widths(monkeypatch, wpl, pipe):
     """Every golden walk case with the multi-sweep tiles forced to 1 and to 2
-    words per lane, and to 1 or 2 tiles per block (the library picks per
-    lattice and launch size; all must be exact)."""
+    words per lane, and with one block per tile or the persistent pipelined
+    kernel (the library picks per lattice and launch size; all must be
+    exact)."""
     monkeypatch.setenv("TSB_DOM_WPL", str(wpl))
-    monkeypatch.setenv("TSB_DOM_TPC", str(tpc))
+    monkeypatch.setenv("TSB_DOM_PIPE", str(pipe))
     monkeypatch.setenv("TSB_DOM_RESIDENT", "0")  # the tiled kernels, even for the small cases
     g = np.load(os.path.join(G, "domino_walks.npz"))
     i = 0
@@ -321,7 +322,7 @@ def test_golden_walks_both_tile_widths(monkeypatch, wpl, tpc):
         h.set_plan(plan)
         h.upload(start)
         h.walk([5, 6], steps)
-        assert np.array_equal(h.download(), oracle.domino_walk(start, [5, 6], plan.p_up, steps)), (order, wpl, tpc)
+        assert np.array_equal(h.download(), oracle.domino_walk(start, [5, 6], plan.p_up, steps)), (order, wpl, pipe)
 
 
 @pytest.mark.parametrize("mode", ["0", "1"])

@@ -12,5 +12,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:domino_multi -s 100 -c 2 -o gpurun_out/prof_multi_warm python bench.py $ARGS > gpurun_out/prof_full.txt 2>&1
 timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:sv_multi -s 200 -c 1 -o gpurun_out/prof_sv_warm python tools/prof_driver.py sv > gpurun_out/prof_sv.txt 2>&1
 timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:lz_multi -s 200 -c 1 -o gpurun_out/prof_lz_warm python tools/prof_driver.py lz > gpurun_out/prof_lz.txt 2>&1
-timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:domino_multi2t -s 20 -c 1 -o gpurun_out/prof_multi2t python tools/dbg_sizes.py 16384 > gpurun_out/prof_multi2t.txt 2>&1
+timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:domino_multi_pipe -s 20 -c 1 -o gpurun_out/prof_multi_pipe python tools/dbg_sizes.py 16384 > gpurun_out/prof_multi_pipe.txt 2>&1
 timeout 1200 python tools/bench_configs.py --only strips,batched > gpurun_out/configs_extra.txt 2>&1

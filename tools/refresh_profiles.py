@@ -40,12 +40,12 @@ def main():
     summ("prof_lz_warm.ncu-rep",
          "ncu --set full --clock-control none --cache-control none --import-source on -k regex:lz_multi -s 200 -c 1 python tools/prof_driver.py lz",
          "round1_lz_multi_ncu.txt", "lz_multi_kernel<0> (4 sweeps/launch, band-aligned tiles), lozenge hexagon 1000^3 q=0.999 after 2000 sweeps from T_min")
-    if os.path.exists(os.path.join(G, "prof_multi2t.ncu-rep")):
-        summ("prof_multi2t.ncu-rep",
-             "ncu --set full --clock-control none --cache-control none --import-source on -k regex:domino_multi2t -s 20 -c 1 python tools/dbg_sizes.py 16384",
-             "round1_domino_multi2t_ncu.txt",
-             "domino_multi2t_kernel<0> (2 sweeps/launch, two prefetched tiles per block), C4 lattice Aztec 16384 from T_max "
-             "after 256 sweeps (HBM-streaming: 2 x 285 MB state buffers)")
+    if os.path.exists(os.path.join(G, "prof_multi_pipe.ncu-rep")):
+        summ("prof_multi_pipe.ncu-rep",
+             "ncu --set full --clock-control none --cache-control none --import-source on -k regex:domino_multi_pipe -s 20 -c 1 python tools/dbg_sizes.py 16384",
+             "round1_domino_multi_pipe_ncu.txt",
+             "domino_multi_pipe_kernel<0> (2 sweeps/launch, persistent blocks, next tile fetched by cp.async), C4 lattice "
+             "Aztec 16384 from T_max after 256 sweeps (HBM-streaming: 2 x 285 MB state buffers)")
     if os.path.exists(os.path.join(G, "configs_extra.txt")):
         extra = [ln for ln in open(os.path.join(G, "configs_extra.txt")).read().splitlines() if ln.startswith("{")]
         strips = [ln for ln in extra if json.loads(ln)["config"].startswith("strips")]
