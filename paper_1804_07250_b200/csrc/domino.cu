@@ -38,7 +38,7 @@ constexpr int kPad = 2;         // zero words left of every state row (lane 0's 
 constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
-constexpr int kPipeMinTiles = 12288;    // launches of at least this many tiles use the pipelined kernel
+constexpr int kPipeMinTiles = 5000;     // launches of at least this many tiles use the pipelined kernel
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
@@ -774,11 +774,12 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
         }
         return TSB_OK;
     }
-    // Launches that stream more tiles than L2 holds (>= kPipeMinTiles x 8 KB
-    // loaded) use the persistent cp.async-pipelined kernel: Aztec 12288 36.0
-    // -> 29.1 us per sweep, C4 (Aztec 16384) 61.7 -> 51.3.  L2-resident
-    // launches keep one short-lived block per tile (pipelining Aztec 4096:
-    // 6.1 -> 7.1 us; its time is set by the slowest RNG-heavy tiles).
+    // Launches of >= kPipeMinTiles tiles (>= 40 MB loaded, state beyond L2)
+    // use the persistent cp.async-pipelined kernel: Aztec 12288 36.0 -> 29.1
+    // us per sweep, C4 (Aztec 16384) 61.7 -> 51.3, its 1/2 and 1/4 strip
+    // windows 34.4 -> 28.0 and 15.7 -> 14.4.  Smaller launches keep one
+    // short-lived block per tile (pipelined: 1/8 window 9.7 -> 9.8, Aztec
+    // 4096 6.1 -> 7.1 us; their time is set by the slowest RNG-heavy tiles).
     const bool big = (size_t)h->win_mn * (size_t)n >= (size_t)kPipeMinTiles;
     if (h->m_pipe == 1 || (h->m_pipe < 0 && big)) {
         cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
