@@ -607,6 +607,28 @@ def loz_cftp(domain: TriDomain, weights, master_seed: int, backend: Backend | No
     return results[0] if count == 1 else results
 
 
+def loz_cftp_distributed(domain: TriDomain, weights, master_seed: int, count: int, group=None,
+                         max_doublings: int = 40) -> list[LozengeTiling]:
+    """loz_cftp(..., count=count) with the samples spread round-robin over the
+    ranks of a torch.distributed group (cftp.distribute_samples); equal to
+    the one-GPU result.  Every rank returns the full list."""
+    from .cftp import distribute_samples
+
+    weights = weights or Uniform()
+    extremals = loz_extremal(domain)
+    if extremals is None:
+        raise UntileableDomain("triangle domain is not tileable")
+    t_max, t_min = extremals
+    if np.array_equal(t_max.edges, t_min.edges):
+        return [t_max] * count
+
+    def run(mine):
+        masters = np.array([chain_master_seed(master_seed, k) for k in mine], dtype=np.uint64)
+        return _loz_cftp_device(domain, weights, t_max.edges, t_min.edges, masters, max_doublings, None, None)
+
+    return [LozengeTiling(domain, e) for e in distribute_samples(count, run, group)]
+
+
 def _loz_cftp_device(domain, weights, top0, bot0, masters, max_doublings, progress, trace):
     from .sixvertex import _fill_trace
 

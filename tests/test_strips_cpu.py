@@ -85,3 +85,30 @@ def test_strip_bounds_balance():
     assert max(per) - min(per) <= 2 * (d.n + 1)  # within one row of perfect balance
     with pytest.raises(ValueError):
         strip_bounds(d.vertex_mask, 200, min_rows=8)
+
+
+def _replica_worker(rank, world, port, out_dir):
+    from paper_1804_07250_b200.cftp import distribute_samples
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    seen = []
+
+    def run(mine):
+        seen.extend(mine)
+        return [np.full(3, k * k, dtype=np.int64) for k in mine]
+
+    out = distribute_samples(7, run)
+    np.save(os.path.join(out_dir, f"rep{rank}.npy"), np.stack(out))
+    np.save(os.path.join(out_dir, f"mine{rank}.npy"), np.array(seen))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cftp_replicas_round_robin(tmp_path, world):
+    """distribute_samples (the CFTP replica layer of all three models): rank r
+    runs samples r, r + world, ...; every rank gets all results in order."""
+    mp.spawn(_replica_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    want = np.stack([np.full(3, k * k, dtype=np.int64) for k in range(7)])
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"rep{r}.npy"), want)
+        assert list(np.load(tmp_path / f"mine{r}.npy")) == list(range(r, 7, world))

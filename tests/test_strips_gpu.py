@@ -157,3 +157,31 @@ def test_cftp_samples_spread_over_processes(tmp_path):
     d = ts.Domain.aztec(10)
     ref = np.stack([t.states for t in ts.cftp_sample_many(d, ts.SweepPlan(d), 0xC0FFEE, 7)])
     assert np.array_equal(np.load(tmp_path / "cftp.npy"), ref)
+
+
+def _cftp_models_worker(rank, world, port, out_dir):
+    import paper_1804_07250_b200 as ts
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    loz = ts.loz_cftp_distributed(ts.TriDomain.hexagon(3, 2, 4), ts.VolumeWeights(0.8), 77, 5)
+    sv = ts.sv_cftp_distributed(6, ts.dwbc(6), ts.SVWeights(1.0, 1.0, 1.5), 2024, 5)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "loz.npy"), np.stack([t.edges for t in loz]))
+        np.save(os.path.join(out_dir, "sv.npy"), np.stack([np.concatenate([c.h_edges.ravel(), c.v_edges.ravel()])
+                                                           for c in sv]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_lozenge_and_sixvertex_cftp_spread_over_processes(tmp_path):
+    """loz_cftp / sv_cftp samples spread round-robin over 2 ranks equal the
+    one-GPU runs (replicas: coupled pairs never leave their GPU)."""
+    import paper_1804_07250_b200 as ts
+
+    mp.spawn(_cftp_models_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    loz = ts.loz_cftp(ts.TriDomain.hexagon(3, 2, 4), ts.VolumeWeights(0.8), 77, count=5)
+    sv = ts.sv_cftp(6, ts.dwbc(6), ts.SVWeights(1.0, 1.0, 1.5), 2024, count=5)
+    assert np.array_equal(np.load(tmp_path / "loz.npy"), np.stack([t.edges for t in loz]))
+    assert np.array_equal(np.load(tmp_path / "sv.npy"),
+                          np.stack([np.concatenate([c.h_edges.ravel(), c.v_edges.ravel()]) for c in sv]))
