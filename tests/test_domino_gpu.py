@@ -342,3 +342,17 @@ def test_resident_and_tiled_paths(monkeypatch, mode):
     seeds = np.arange(1, 21, dtype=np.uint64)
     out = ts.random_walk_batch(start, seeds, 301, plan)
     assert np.array_equal(out, oracle.domino_walk(start, seeds, plan.p_up, 301))
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2), (2, 3), (4, 31), (3, 32), (2, 64)])
+def test_tiny_rectangles_vs_oracle(monkeypatch, mode, rows, cols):
+    """Rectangles down to a single domino and widths at 32-column word edges,
+    through the resident walk (1) and the tiled kernels (0)."""
+    monkeypatch.setenv("TSB_DOM_RESIDENT", mode)
+    d = ts.Domain.rectangle(rows, cols)
+    plan = ts.SweepPlan(d, ts.VolumeWeights(0.6))
+    t_max, t_min = ts.extremal_tilings(d)
+    start = np.stack([t_max.states, t_min.states])
+    out = ts.random_walk_batch(start, [9, 10], 97, plan)
+    assert np.array_equal(out, oracle.domino_walk(start, [9, 10], plan.p_up, 97))

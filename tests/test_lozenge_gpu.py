@@ -154,3 +154,19 @@ def test_hexagon_arctic_circle_statistics():
     assert frozen.max() < 0.05, frozen.max()
     inner = dens[:, vm & (r < 0.5 * inr)]
     assert np.all(np.abs(inner.mean(axis=1) - 1.0 / 3.0) < 0.05), inner.mean(axis=1)
+
+
+@pytest.mark.parametrize("abc", [(1, 1, 1), (2, 15, 16), (3, 16, 16), (1, 31, 2), (5, 5, 27), (30, 2, 3)])
+def test_thin_hexagons_vs_oracle(abc):
+    """Thin and unbalanced hexagons (vertex columns at and across 32-bit word
+    edges, few-row domains); the extremal states differ, so the walk moves."""
+    d = ts.TriDomain.hexagon(*abc)
+    t_max, t_min = ts.loz_extremal(d)
+    assert not np.array_equal(t_max.edges, t_min.edges)
+    start = np.stack([t_min.edges, t_max.edges])
+    seeds = np.array([21, 22], dtype=np.uint64)
+    w = ts.VolumeWeights(1.3)
+    out = loz_random_walk_batch(start, seeds, 123, d, w)
+    assert np.array_equal(out, oracle.loz_walk(start, seeds, loz_p_up_grid(d, w), 123))
+    if sum(abc) > 10:  # (1, 1, 1) has two tilings: it may well end where it started
+        assert not np.array_equal(out[0], start[0])

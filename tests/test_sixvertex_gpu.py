@@ -152,3 +152,17 @@ def test_large_batch_uses_batch_geometry():
     h.upload(start)
     h.walk(seeds, steps)
     assert np.array_equal(h.download(), oracle.sv_walk(start, seeds, w.table(), steps))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 32, 33])
+def test_tiny_and_word_edge_sizes_vs_oracle(n):
+    """DWBC sizes with no interior face (n = 1), a single one, and face grids
+    one word wide or straddling a word boundary (32 / 33 / 34 columns)."""
+    hi, lo = closed_form(n)
+    start = np.stack([lo, hi]).astype(np.int32)
+    seeds = np.array([3, 4], dtype=np.uint64)
+    w = ts.SVWeights(0.8, 1.1, 1.7)
+    out = sv_random_walk_batch(start, seeds, 150, w)
+    assert np.array_equal(out, oracle.sv_walk(start, seeds, w.table(), 150))
+    if n == 1:
+        assert np.array_equal(out, start)
