@@ -180,7 +180,7 @@ constexpr size_t sv_multi_smem() {
     return sizeof(uint32_t) * (2 * NW) * (32 * WPL)    // rows
            + sizeof(uint64_t) * 32                      // lut
            + sizeof(uint32_t) * NW * (32 * WPL)         // per-warp flip words
-           + sizeof(uint32_t) * NW * (32 * WPL) * 16;   // per-warp job queues
+           + sizeof(uint16_t) * NW * (32 * WPL) * 16;   // per-warp job queues
 }
 
 template <int WPL, int NW>
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
     uint64_t *lut = reinterpret_cast<uint64_t *>(dsm + sizeof(uint32_t) * TR * TW);
     uint32_t *fres = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32) +
                      (threadIdx.x >> 5) * TW;
-    uint32_t *queue = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32 +
+    uint16_t *queue = reinterpret_cast<uint16_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32 +
                                                    sizeof(uint32_t) * NW * TW) +
                       (threadIdx.x >> 5) * TW * 16;
     const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             int pos = incl - cnt;
-            // job = li << 12 | lane << 7 | j << 5 | bit;  li = (up ? 0 : 16) | nw<<3 | ne<<2 | sw<<1 | se
+            // job = li << 11 | lane << 6 | j << 4 | bit >> 1 (16 bits: a class sweep's sites all have
+            // bit parity pc);  li = (up ? 0 : 16) | nw<<3 | ne<<2 | sw<<1 | se
 #pragma unroll
             for (int j = 0; j < WPL; ++j) {
                 for (uint32_t m = cand[j]; m; m &= m - 1) {
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
                     const uint32_t li = (((mn[j] >> bt) & 1u) ? 0u : 16u) | (((nw[j] >> bt) & 1u) << 3) |
                                         (((ne[j] >> bt) & 1u) << 2) | (((sw[j] >> bt) & 1u) << 1) |
                                         ((se[j] >> bt) & 1u);
-                    queue[pos++] = (li << 12) | ((uint32_t)lane << 7) | ((uint32_t)j << 5) | (uint32_t)bt;
+                    queue[pos++] = (uint16_t)((li << 11) | ((uint32_t)lane << 6) | ((uint32_t)j << 4) | ((uint32_t)bt >> 1));
                 }
                 fres[lane * WPL + j] = 0u;
             }
@@ -305,15 +306,15 @@ __global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
             for (int q = lane; q < total; q += 64) {
                 const bool two = q + 32 < total;
                 const uint32_t j0 = queue[q], j1 = two ? queue[q + 32] : j0;
-                const uint64_t i0 = row_idx + (uint64_t)((((j0 >> 7) & 31u) * WPL + ((j0 >> 5) & 3u)) * 32u + (j0 & 31u));
-                const uint64_t i1 = row_idx + (uint64_t)((((j1 >> 7) & 31u) * WPL + ((j1 >> 5) & 3u)) * 32u + (j1 & 31u));
+                const uint32_t w0 = ((j0 >> 6) & 31u) * WPL + ((j0 >> 4) & 3u), b0 = ((j0 & 15u) << 1) | (uint32_t)pc;
+                const uint32_t w1 = ((j1 >> 6) & 31u) * WPL + ((j1 >> 4) & 3u), b1 = ((j1 & 15u) << 1) | (uint32_t)pc;
+                const uint64_t i0 = row_idx + (uint64_t)(w0 * 32u + b0);
+                const uint64_t i1 = row_idx + (uint64_t)(w1 * 32u + b1);
                 const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
                 const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
                 // local min (up) moves iff u < p_high; local max moves iff u >= p_high
-                if (((x0 >> 11) < lut[j0 >> 12]) == !((j0 >> 16) & 1u))
-                    atomicOr(&fres[((j0 >> 7) & 31u) * WPL + ((j0 >> 5) & 3u)], 1u << (j0 & 31u));
-                if (two && ((x1 >> 11) < lut[j1 >> 12]) == !((j1 >> 16) & 1u))
-                    atomicOr(&fres[((j1 >> 7) & 31u) * WPL + ((j1 >> 5) & 3u)], 1u << (j1 & 31u));
+                if (((x0 >> 11) < lut[j0 >> 11]) == !((j0 >> 15) & 1u)) atomicOr(&fres[w0], 1u << b0);
+                if (two && ((x1 >> 11) < lut[j1 >> 11]) == !((j1 >> 15) & 1u)) atomicOr(&fres[w1], 1u << b1);
             }
             __syncwarp();
 #pragma unroll
@@ -528,13 +529,21 @@ static int sv_k(const tsb_sv *h, int n) {
     return blocks >= 2 * (int64_t)h->m_sms ? 4 : 8;
 }
 
+// A launch of at most one block per SM reserves more than half an SM's
+// shared memory per block, so the scheduler spreads the blocks over all SMs
+// instead of packing two onto one (single chains of the DWBC 2048 lattice:
+// 129 blocks); larger launches pack as tightly as registers allow.
+constexpr size_t kSvSpreadSmem = 116 * 1024;
+
 template <int WPL, int NW>
-static int sv_launch_multi_t(const cudaLaunchConfig_t &cfg0, const SvMCtx &c) {
+static int sv_launch_multi_t(const cudaLaunchConfig_t &cfg0, const SvMCtx &c, int sms) {
     constexpr size_t smem = sv_multi_smem<WPL, NW>();
-    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t blocks = (size_t)cfg0.gridDim.x * cfg0.gridDim.y * cfg0.gridDim.z;
+    const size_t use = blocks <= (size_t)sms ? std::max(smem, kSvSpreadSmem) : smem;
+    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
     cudaLaunchConfig_t cfg = cfg0;
     cfg.blockDim = dim3(32 * NW);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = use;
     TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW>, c));
     return TSB_OK;
 }
@@ -569,14 +578,14 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
     cfg.numAttrs = 1;
     const int key = h->m_wpl * 100 + h->m_nw;
     switch (key) {
-        case 108: return sv_launch_multi_t<1, 8>(cfg, c);
-        case 208: return sv_launch_multi_t<2, 8>(cfg, c);
-        case 308: return sv_launch_multi_t<3, 8>(cfg, c);
-        case 408: return sv_launch_multi_t<4, 8>(cfg, c);
-        case 116: return sv_launch_multi_t<1, 16>(cfg, c);
-        case 216: return sv_launch_multi_t<2, 16>(cfg, c);
-        case 316: return sv_launch_multi_t<3, 16>(cfg, c);
-        default: return sv_launch_multi_t<4, 16>(cfg, c);
+        case 108: return sv_launch_multi_t<1, 8>(cfg, c, h->m_sms);
+        case 208: return sv_launch_multi_t<2, 8>(cfg, c, h->m_sms);
+        case 308: return sv_launch_multi_t<3, 8>(cfg, c, h->m_sms);
+        case 408: return sv_launch_multi_t<4, 8>(cfg, c, h->m_sms);
+        case 116: return sv_launch_multi_t<1, 16>(cfg, c, h->m_sms);
+        case 216: return sv_launch_multi_t<2, 16>(cfg, c, h->m_sms);
+        case 316: return sv_launch_multi_t<3, 16>(cfg, c, h->m_sms);
+        default: return sv_launch_multi_t<4, 16>(cfg, c, h->m_sms);
     }
 }
 

@@ -14,7 +14,7 @@ for i in 1 2; do
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
-        d=json.loads(l); print(d['config'][:50], {k: round(v,3) for k,v in d.items() if k in ('us_per_sweep','chain_sweeps_per_s','rotateable_fraction')})" >> gpurun_out/ab_multi.txt 2>&1
+        d=json.loads(l); print(d['config'][:50], {k: round(v,3) for k,v in d.items() if k in ('us_per_sweep','chain_sweeps_per_s','rotateable_fraction','us_per_sweep_all_chains','roofline_frac')})" >> gpurun_out/ab_multi.txt 2>&1
   done
 done
 unset TSB_LIB
