@@ -27,6 +27,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
 #include "domino.cuh"
 #include "tsb_fire.cuh"
 
@@ -55,6 +58,8 @@ struct SweepCtx {
     int side, pitch;
     uint64_t step;
     int color_override;  // -1: colour from the global coin (direct launches)
+    const int *order;    // multi-sweep adaptive order: canonical index of the tile of block b (tiles permuted)
+    unsigned *cost;      // multi-sweep: per-tile block duration in cycles (null: not measured)
 };
 
 // One sweep, one block per non-empty tile of kTileRows x 62 words (512
@@ -236,9 +241,10 @@ template <int TM>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
     TT(0);
     MULTI_SMEM;
+    __shared__ long long t_start;
     const int lane = threadIdx.x & 31;
     const int k = threadIdx.x >> 5;
-    const int2 tile = c.tiles[blockIdx.x];
+    const int2 tile = c.tiles[blockIdx.x];  // adaptive order: c.tiles is the permuted list
     const int r = tile.y * kMOut - kMK + k;
     const int wa = tile.x + 2 * lane;  // band-aligned tile: tile.x = first loaded word (even)
     const int z = blockIdx.z;
@@ -248,9 +254,11 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     TT(1);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     TT(2);
+    if (c.cost && threadIdx.x == 0) t_start = clock64();
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
     if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
     multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur, *c.step_dev + c.step);
+    if (c.cost && threadIdx.x == 0) c.cost[c.order[blockIdx.x]] = (unsigned)(clock64() - t_start);  // after the last barrier
     TT(5);
 }
 
@@ -706,6 +714,8 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     c.pitch = h->pitch;
     c.step = step;
     c.color_override = color_override;
+    c.order = nullptr;
+    c.cost = nullptr;
     h->cur ^= 1;
     if (h->ntiles == 0) return TSB_OK;
     cudaLaunchConfig_t cfg = {};
@@ -724,6 +734,17 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
         default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_sweep_kernel<2>, c)); break;
     }
     return TSB_OK;
+}
+
+static bool pipe_launch(const tsb_domino *h, int n) {
+    return h->m_pipe == 1 || (h->m_pipe < 0 && (size_t)h->win_mn * (size_t)n >= (size_t)kPipeMinTiles);
+}
+
+// Whole-domain launches of the one-block-per-tile kernel use the adaptive
+// dispatch order (order_kernel); TSB_DOM_ADAPT=0 keeps band-major order.
+static bool adaptive_order(const tsb_domino *h, int n) {
+    return h->m_order && h->m_adapt && h->m_wpl == 2 && !h->coupled && h->win_m0 == 0 &&
+           h->win_mn == h->nmtiles && !pipe_launch(h, n);
 }
 
 // kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
@@ -745,6 +766,10 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     c.pitch = h->pitch;
     c.step = step_off;
     c.color_override = -1;
+    const bool adapt = adaptive_order(h, n);
+    c.order = adapt ? h->m_order : nullptr;
+    c.cost = adapt ? h->m_cost : nullptr;
+    if (adapt) c.tiles = h->m_perm;
     h->cur ^= 1;
     if (h->win_mn == 0) return TSB_OK;
     cudaLaunchConfig_t cfg = {};
@@ -780,8 +805,7 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     // windows 34.4 -> 28.0 and 15.7 -> 14.4.  Smaller launches keep one
     // short-lived block per tile (pipelined: 1/8 window 9.7 -> 9.8, Aztec
     // 4096 6.1 -> 7.1 us; their time is set by the slowest RNG-heavy tiles).
-    const bool big = (size_t)h->win_mn * (size_t)n >= (size_t)kPipeMinTiles;
-    if (h->m_pipe == 1 || (h->m_pipe < 0 && big)) {
+    if (pipe_launch(h, n)) {
         cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
         cfg.dynamicSmemBytes = kPipeSmem;
         switch (h->tmode) {
@@ -801,6 +825,55 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
 
 __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
 __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
+
+// Adaptive dispatch order of whole-domain multi-sweep launches (end of every
+// graph replay).  Each block records how long its tile took (cycles, thread
+// 0, after the last barrier); tiles are then dispatched by cost class --
+// more than 3x the mean duration, 1.5x, 1x, the rest --
+// and in band-major order within a class.  The slow tiles are those whose
+// rows hold many rotateable sites (long coin queues: the melting seam of an
+// Aztec diamond started from T_max, the disordered disk of a mixed state);
+// dispatched first they no longer start mid-launch and set its end, while
+// band-major order within a class keeps neighbouring bands together.
+// Results do not depend on the order.
+constexpr int kOrderThreads = 1024;
+constexpr int kOrderClasses = 4;
+
+__device__ __forceinline__ int cost_class(unsigned cost, int n, unsigned long long tot) {
+    const unsigned long long x = 2ull * (unsigned long long)cost * (unsigned long long)n;  // 2 * cost / mean * tot
+    return x > 6ull * tot ? 3 : x > 3ull * tot ? 2 : x > 2ull * tot ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *cost, const int2 *tiles, int n,
+                                                                int *order, int2 *perm) {
+    typedef cub::BlockReduce<unsigned long long, kOrderThreads> Reduce;
+    typedef cub::BlockScan<int, kOrderThreads> Scan;
+    __shared__ union {
+        typename Reduce::TempStorage r;
+        typename Scan::TempStorage s;
+    } tmp;
+    __shared__ unsigned long long tot_s;
+    unsigned long long part = 0;
+    for (int i = threadIdx.x; i < n; i += kOrderThreads) part += cost[i];
+    const unsigned long long tot = Reduce(tmp.r).Sum(part);
+    if (threadIdx.x == 0) tot_s = tot;
+    __syncthreads();
+    int pos = 0;  // block-uniform
+    for (int cls = kOrderClasses - 1; cls >= 0; --cls) {
+        for (int i0 = 0; i0 < n; i0 += kOrderThreads) {
+            const int i = i0 + threadIdx.x;
+            const int f = i < n && cost_class(cost[i], n, tot_s) == cls;
+            int o, t;
+            __syncthreads();
+            Scan(tmp.s).ExclusiveSum(f, o, t);
+            if (f) {
+                order[pos + o] = i;
+                perm[pos + o] = tiles[i];
+            }
+            pos += t;
+        }
+    }
+}
 
 // A CUDA graph of kGraphSweeps sweeps (even, so the buffers end where they
 // started) followed by `step += kGraphSweeps`; long walks replay it, which
@@ -823,6 +896,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
+    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost, h->mtiles, h->nmtiles, h->m_order, h->m_perm);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
     if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -1004,6 +1078,20 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     if (!mtiles.empty() &&
         (e = cudaMemcpy(h->mtiles, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
         return bail(e, "mtiles");
+    {
+        std::vector<int> iota(std::max<size_t>(1, mtiles.size()));
+        for (size_t i = 0; i < iota.size(); ++i) iota[i] = (int)i;
+        if ((e = cudaMalloc(&h->m_order, sizeof(int) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc order");
+        if ((e = cudaMemcpy(h->m_order, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(e, "order");
+        if ((e = cudaMalloc(&h->m_perm, sizeof(int2) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc perm");
+        if (!mtiles.empty() &&
+            (e = cudaMemcpy(h->m_perm, mtiles.data(), sizeof(int2) * mtiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(e, "perm");
+        if ((e = cudaMalloc(&h->m_cost, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc cost");
+        if ((e = cudaMemset(h->m_cost, 0, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cost");
+        if (const char *ev = getenv("TSB_DOM_ADAPT")) h->m_adapt = atoi(ev) != 0;
+    }
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
                            (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
                            (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>,
@@ -1037,6 +1125,9 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->range);
     cudaFree(h->tiles);
     cudaFree(h->mtiles);
+    cudaFree(h->m_order);
+    cudaFree(h->m_perm);
+    cudaFree(h->m_cost);
     cudaFree(h->tgrid);
     cudaFree(h->seedinfo);
     cudaFree(h->bytes);

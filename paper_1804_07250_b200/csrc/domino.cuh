@@ -19,6 +19,10 @@ struct tsb_domino {
     int win_t0 = 0, win_tn = 0;   // swept tile range (row window; default all)
     int2 *mtiles = nullptr;       // tiles of the temporally blocked kernel (kMOut-row bands)
     int nmtiles = 0;
+    int *m_order = nullptr;       // dispatch order of whole-domain multi-sweep launches (order_kernel)
+    unsigned *m_cost = nullptr;   // last block duration per multi-sweep tile (cycles)
+    int2 *m_perm = nullptr;       // mtiles in that order
+    bool m_adapt = true;          // TSB_DOM_ADAPT=0: band-major order
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
     int m_pipe = -1;  // 2-word multi-sweep kernel: -1 auto, 0 one block per tile, 1 persistent pipelined (TSB_DOM_PIPE)

@@ -356,3 +356,18 @@ def test_tiny_rectangles_vs_oracle(monkeypatch, mode, rows, cols):
     start = np.stack([t_max.states, t_min.states])
     out = ts.random_walk_batch(start, [9, 10], 97, plan)
     assert np.array_equal(out, oracle.domino_walk(start, [9, 10], plan.p_up, 97))
+
+
+@pytest.mark.parametrize("adapt", ["0", "1"])
+def test_adaptive_dispatch_order_is_exact(monkeypatch, adapt):
+    """Whole-domain walks long enough for several reorderings of the tile
+    dispatch (one per 64-sweep graph replay, by measured block durations)
+    equal the oracle, with the adaptive order on and off."""
+    monkeypatch.setenv("TSB_DOM_ADAPT", adapt)
+    monkeypatch.setenv("TSB_DOM_RESIDENT", "0")
+    d = ts.Domain.aztec(300)
+    plan = ts.SweepPlan(d)
+    t_max, t_min = ts.extremal_tilings(d)
+    start = t_max.states[None]
+    out = ts.random_walk_batch(start, [0x5EED], 1000, plan)
+    assert np.array_equal(out, oracle.domino_walk(start, [0x5EED], plan.p_up, 1000))
