@@ -278,7 +278,6 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 template <int TM>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(SweepCtx c) {
     MULTI_SMEM;
-    __shared__ long long t_start;
     uint4 *slot = reinterpret_cast<uint4 *>(dsm + kMSmem) + threadIdx.x;  // [2][blockDim]
     const int lane = threadIdx.x & 31;
     const int k = threadIdx.x >> 5;
@@ -308,9 +307,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
         const uint4 cur = slot[b * 32 * kMRows];
         const int2 t = c.tiles[i];
         const int r = t.y * kMOut - kMK + k;
-        if (c.cost && threadIdx.x == 0) t_start = clock64();
         multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
-        if (c.cost && threadIdx.x == 0) c.cost[c.order[i]] = (unsigned)(clock64() - t_start);
     }
 }
 
@@ -747,7 +744,7 @@ static bool pipe_launch(const tsb_domino *h, int n) {
 // dispatch order (order_kernel); TSB_DOM_ADAPT=0 keeps band-major order.
 static bool adaptive_order(const tsb_domino *h, int n) {
     return h->m_order && h->m_adapt && h->m_wpl == 2 && !h->coupled && h->win_m0 == 0 &&
-           h->win_mn == h->nmtiles && (h->m_adapt_pipe || !pipe_launch(h, n));
+           h->win_mn == h->nmtiles && !pipe_launch(h, n);
 }
 
 // kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
@@ -1094,7 +1091,6 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         if ((e = cudaMalloc(&h->m_cost, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc cost");
         if ((e = cudaMemset(h->m_cost, 0, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cost");
         if (const char *ev = getenv("TSB_DOM_ADAPT")) h->m_adapt = atoi(ev) != 0;
-        if (const char *ev = getenv("TSB_DOM_ADAPT_PIPE")) h->m_adapt_pipe = atoi(ev) != 0;
     }
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
                            (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
