@@ -42,6 +42,10 @@ constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per b
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
 constexpr int kPipeMinTiles = 5000;     // launches of at least this many tiles use the pipelined kernel
+constexpr int kOrderThreads = 1024;     // adaptive dispatch order (order_kernel): one block
+constexpr int kOrderClasses = 4;
+constexpr int kOrderPer = 5;            // tiles per thread (whole-domain adaptive launches have < kPipeMinTiles)
+static_assert(kPipeMinTiles <= kOrderThreads * kOrderPer, "order_kernel covers every tile");
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
@@ -744,7 +748,7 @@ static bool pipe_launch(const tsb_domino *h, int n) {
 // dispatch order (order_kernel); TSB_DOM_ADAPT=0 keeps band-major order.
 static bool adaptive_order(const tsb_domino *h, int n) {
     return h->m_order && h->m_adapt && h->m_wpl == 2 && !h->coupled && h->win_m0 == 0 &&
-           h->win_mn == h->nmtiles && !pipe_launch(h, n);
+           h->win_mn == h->nmtiles && !pipe_launch(h, n) && h->nmtiles <= kOrderThreads * kOrderPer;
 }
 
 // kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
@@ -827,7 +831,7 @@ __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v;
 __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
 
 // Adaptive dispatch order of whole-domain multi-sweep launches (end of every
-// graph replay).  Each block records how long its tile took (cycles, thread
+// 4th graph replay: the heavy tiles move slowly).  Each block records how long its tile took (cycles, thread
 // 0, after the last barrier); tiles are then dispatched by cost class --
 // more than 3x the mean duration, 1.5x, 1x, the rest --
 // and in band-major order within a class.  The slow tiles are those whose
@@ -836,8 +840,6 @@ __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev
 // dispatched first they no longer start mid-launch and set its end, while
 // band-major order within a class keeps neighbouring bands together.
 // Results do not depend on the order.
-constexpr int kOrderThreads = 1024;
-constexpr int kOrderClasses = 4;
 
 __device__ __forceinline__ int cost_class(unsigned cost, int n, unsigned long long tot) {
     const unsigned long long x = 2ull * (unsigned long long)cost * (unsigned long long)n;  // 2 * cost / mean * tot
@@ -845,7 +847,10 @@ __device__ __forceinline__ int cost_class(unsigned cost, int n, unsigned long lo
 }
 
 __global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *cost, const int2 *tiles, int n,
-                                                                int *order, int2 *perm) {
+                                                                const uint64_t *step_dev, int every, int *order,
+                                                                int2 *perm) {
+    // the heavy tiles move slowly: reorder on every `every`-th replay only
+    if ((*step_dev / kGraphSweeps) % (uint64_t)every != 0) return;
     typedef cub::BlockReduce<unsigned long long, kOrderThreads> Reduce;
     typedef cub::BlockScan<int, kOrderThreads> Scan;
     __shared__ union {
@@ -853,25 +858,37 @@ __global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *co
         typename Scan::TempStorage s;
     } tmp;
     __shared__ unsigned long long tot_s;
+    // thread t owns tiles kOrderPer * t .. kOrderPer * t + kOrderPer - 1 (one load each)
+    const int i0 = kOrderPer * threadIdx.x;
+    unsigned c[kOrderPer];
     unsigned long long part = 0;
-    for (int i = threadIdx.x; i < n; i += kOrderThreads) part += cost[i];
+#pragma unroll
+    for (int j = 0; j < kOrderPer; ++j) {
+        c[j] = i0 + j < n ? cost[i0 + j] : 0u;
+        part += c[j];
+    }
     const unsigned long long tot = Reduce(tmp.r).Sum(part);
     if (threadIdx.x == 0) tot_s = tot;
     __syncthreads();
+    int cls[kOrderPer];
+#pragma unroll
+    for (int j = 0; j < kOrderPer; ++j) cls[j] = i0 + j < n ? cost_class(c[j], n, tot_s) : -1;
     int pos = 0;  // block-uniform
-    for (int cls = kOrderClasses - 1; cls >= 0; --cls) {
-        for (int i0 = 0; i0 < n; i0 += kOrderThreads) {
-            const int i = i0 + threadIdx.x;
-            const int f = i < n && cost_class(cost[i], n, tot_s) == cls;
-            int o, t;
-            __syncthreads();
-            Scan(tmp.s).ExclusiveSum(f, o, t);
-            if (f) {
-                order[pos + o] = i;
-                perm[pos + o] = tiles[i];
+    for (int k = kOrderClasses - 1; k >= 0; --k) {
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < kOrderPer; ++j) cnt += cls[j] == k;
+        int o, t;
+        __syncthreads();
+        Scan(tmp.s).ExclusiveSum(cnt, o, t);
+#pragma unroll
+        for (int j = 0; j < kOrderPer; ++j)
+            if (cls[j] == k) {
+                order[pos + o] = i0 + j;
+                perm[pos + o] = tiles[i0 + j];
+                ++o;
             }
-            pos += t;
-        }
+        pos += t;
     }
 }
 
@@ -896,7 +913,8 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
-    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost, h->mtiles, h->nmtiles, h->m_order, h->m_perm);
+    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost, h->mtiles, h->nmtiles, h->step_dev,
+                                                          h->m_order_every, h->m_order, h->m_perm);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
     if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -1091,6 +1109,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         if ((e = cudaMalloc(&h->m_cost, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc cost");
         if ((e = cudaMemset(h->m_cost, 0, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cost");
         if (const char *ev = getenv("TSB_DOM_ADAPT")) h->m_adapt = atoi(ev) != 0;
+        if (const char *ev = getenv("TSB_DOM_ORDER_EVERY")) h->m_order_every = std::max(1, atoi(ev));
     }
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
                            (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,

@@ -23,6 +23,7 @@ struct tsb_domino {
     unsigned *m_cost = nullptr;   // last block duration per multi-sweep tile (cycles)
     int2 *m_perm = nullptr;       // mtiles in that order
     bool m_adapt = true;          // TSB_DOM_ADAPT=0: band-major order
+    int m_order_every = 4;        // reorder on every n-th graph replay (TSB_DOM_ORDER_EVERY)
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
     int m_pipe = -1;  // 2-word multi-sweep kernel: -1 auto, 0 one block per tile, 1 persistent pipelined (TSB_DOM_PIPE)
