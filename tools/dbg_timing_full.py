@@ -21,6 +21,9 @@ h.set_plan(ts.SweepPlan(d))
 h.upload(t_max[None])
 h.walk([1], warm)
 h.sync()
+h.walk([1], 512, step0=warm)  # graph replays: the adaptive order settles
+warm += 512
+h.sync()
 L = _native.lib()
 L.tsb_debug_timing.argtypes = [ctypes.c_void_p]
 h.walk([1], 32, step0=warm)  # 16 direct multi-sweep launches (< one graph replay)
