@@ -41,11 +41,10 @@ constexpr int kPad = 2;         // zero words left of every state row (lane 0's 
 constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
-constexpr int kPipeMinTiles = 5000;     // launches of at least this many tiles use the pipelined kernel
+constexpr size_t kPipeMinBytes = 96ull << 20;  // launches whose two state buffers exceed this use the pipelined kernel
 constexpr int kOrderThreads = 1024;     // adaptive dispatch order (order_kernel): one block
 constexpr int kOrderClasses = 4;
-constexpr int kOrderPer = 5;            // tiles per thread (whole-domain adaptive launches have < kPipeMinTiles)
-static_assert(kPipeMinTiles <= kOrderThreads * kOrderPer, "order_kernel covers every tile");
+constexpr int kOrderPer = 8;            // tiles per thread: launches of more tiles use the pipelined kernel
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
 
 struct SweepCtx {
@@ -740,15 +739,24 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     return TSB_OK;
 }
 
+// The pipelined kernel pays off once a launch streams from HBM: the two state
+// buffers of the launched rows exceed what L2 keeps (Aztec 8192 and up, C4
+// windows down to 1/4); L2-resident launches use one short-lived block per tile
+// with the adaptive order (a 1/8 window of Aztec 16384: 9.6 -> 8.0 us/sweep).
 static bool pipe_launch(const tsb_domino *h, int n) {
-    return h->m_pipe == 1 || (h->m_pipe < 0 && (size_t)h->win_mn * (size_t)n >= (size_t)kPipeMinTiles);
+    if (h->m_pipe >= 0) return h->m_pipe == 1;
+    const size_t bytes = 2 * sizeof(uint2) * (size_t)h->win_rows * h->pitch * (size_t)n;
+    return bytes > kPipeMinBytes || (size_t)h->win_mn * (size_t)n > (size_t)kOrderThreads * kOrderPer;
 }
 
 // Whole-domain launches of the one-block-per-tile kernel use the adaptive
 // dispatch order (order_kernel); TSB_DOM_ADAPT=0 keeps band-major order.
 static bool adaptive_order(const tsb_domino *h, int n) {
-    return h->m_order && h->m_adapt && h->m_wpl == 2 && !h->coupled && h->win_m0 == 0 &&
-           h->win_mn == h->nmtiles && !pipe_launch(h, n) && h->nmtiles <= kOrderThreads * kOrderPer;
+    // row windows (strips) only with several waves of tiles: on the ~2-wave
+    // windows of Aztec 4096 heavy-first was slower (1/4 window 4.3 -> 7.1 us)
+    const bool full = h->win_m0 == 0 && h->win_mn == h->nmtiles;
+    return h->m_order && h->m_adapt && h->m_wpl == 2 && !h->coupled && h->win_mn > 0 && !pipe_launch(h, n) &&
+           h->win_mn <= kOrderThreads * kOrderPer && (full || h->win_mn >= 12 * h->num_sms);
 }
 
 // kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
@@ -771,9 +779,10 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     c.step = step_off;
     c.color_override = -1;
     const bool adapt = adaptive_order(h, n);
-    c.order = adapt ? h->m_order : nullptr;
-    c.cost = adapt ? h->m_cost : nullptr;
-    if (adapt) c.tiles = h->m_perm;
+    // adaptive order over the launched window: indices relative to its first tile
+    c.order = adapt ? h->m_order + h->win_m0 : nullptr;
+    c.cost = adapt ? h->m_cost + h->win_m0 : nullptr;
+    if (adapt) c.tiles = h->m_perm + h->win_m0;
     h->cur ^= 1;
     if (h->win_mn == 0) return TSB_OK;
     cudaLaunchConfig_t cfg = {};
@@ -803,12 +812,7 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
         }
         return TSB_OK;
     }
-    // Launches of >= kPipeMinTiles tiles (>= 40 MB loaded, state beyond L2)
-    // use the persistent cp.async-pipelined kernel: Aztec 12288 36.0 -> 29.1
-    // us per sweep, C4 (Aztec 16384) 61.7 -> 51.3, its 1/2 and 1/4 strip
-    // windows 34.4 -> 28.0 and 15.7 -> 14.4.  Smaller launches keep one
-    // short-lived block per tile (pipelined: 1/8 window 9.7 -> 9.8, Aztec
-    // 4096 6.1 -> 7.1 us; their time is set by the slowest RNG-heavy tiles).
+    // HBM-streaming launches: the persistent cp.async-pipelined kernel (pipe_launch)
     if (pipe_launch(h, n)) {
         cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
         cfg.dynamicSmemBytes = kPipeSmem;
@@ -829,6 +833,15 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
 
 __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
 __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
+
+// canonical (band-major) order of a window's tiles [0, n): order_kernel input state
+__global__ void order_reset_kernel(const int2 *tiles, int n, int *order, int2 *perm, unsigned *cost) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    order[i] = i;
+    perm[i] = tiles[i];
+    cost[i] = 0u;
+}
 
 // Adaptive dispatch order of whole-domain multi-sweep launches (end of every
 // 4th graph replay: the heavy tiles move slowly).  Each block records how long its tile took (cycles, thread
@@ -913,8 +926,9 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
-    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost, h->mtiles, h->nmtiles, h->step_dev,
-                                                          h->m_order_every, h->m_order, h->m_perm);
+    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost + h->win_m0, h->mtiles + h->win_m0, h->win_mn,
+                                                          h->step_dev, h->m_order_every, h->m_order + h->win_m0,
+                                                          h->m_perm + h->win_m0);
     advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
     if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -1091,6 +1105,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     h->win_tn = h->ntiles;
     h->win_m0 = 0;
     h->win_mn = h->nmtiles;
+    h->win_rows = side;
     if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mtiles.size()))) != cudaSuccess)
         return bail(e, "cudaMalloc mtiles");
     if (!mtiles.empty() &&
@@ -1346,8 +1361,10 @@ int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi) {
     row_hi = std::min(h->side, row_hi);
     if (row_hi <= row_lo) {
         h->win_t0 = h->win_tn = h->win_m0 = h->win_mn = 0;
+        h->win_rows = 0;
         return TSB_OK;
     }
+    h->win_rows = row_hi - row_lo;
     int y0 = row_lo / kTileRows, y1 = (row_hi - 1) / kTileRows;
     h->win_t0 = h->band_start[y0];
     h->win_tn = h->band_start[y1 + 1] - h->win_t0;
@@ -1355,6 +1372,13 @@ int tsb_domino_set_window(tsb_domino *h, int row_lo, int row_hi) {
     y1 = (row_hi - 1) / kMOut;
     h->win_m0 = h->mband_start[y0];
     h->win_mn = h->mband_start[y1 + 1] - h->win_m0;
+    if (h->m_order && h->win_mn > 0) {  // the window's adaptive order starts band-major
+        TSB_CUDA(cudaSetDevice(h->device));
+        order_reset_kernel<<<(h->win_mn + 255) / 256, 256, 0, h->stream>>>(h->mtiles + h->win_m0, h->win_mn,
+                                                                            h->m_order + h->win_m0,
+                                                                            h->m_perm + h->win_m0, h->m_cost + h->win_m0);
+        TSB_CUDA(cudaGetLastError());
+    }
     return TSB_OK;
 }
 

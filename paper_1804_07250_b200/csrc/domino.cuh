@@ -26,6 +26,7 @@ struct tsb_domino {
     int m_order_every = 4;        // reorder on every n-th graph replay (TSB_DOM_ORDER_EVERY)
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
+    int win_rows = 0;  // rows of the swept window (set with the tile lists; default: side)
     int m_pipe = -1;  // 2-word multi-sweep kernel: -1 auto, 0 one block per tile, 1 persistent pipelined (TSB_DOM_PIPE)
     int num_sms = 148;
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
