@@ -34,6 +34,7 @@ constexpr size_t kLzMSmem = sizeof(uint4) * kLzMRows * 32 + sizeof(uint2) * kLzM
 
 struct tsb_loz {
     int device = 0, sx = 0, sy = 0, X = 0, Y = 0, nchains = 0, W = 0, pitch = 0;
+    int m_sms = 148, m_dense = -1;  // SM count; 3-blocks-per-SM kernel: -1 auto (multi-wave batches), 0/1 (TSB_LZ_DENSE)
     size_t plane = 0;        // u32 per plane (incl. guard rows)
     size_t chain_words = 0;  // 3 planes
     uint32_t *buf[2] = {nullptr, nullptr};
@@ -211,8 +212,8 @@ struct LzMCtx {
 // (pull-form updates).  Rows / bits next to the unloaded outside go stale by
 // one per sweep, so the central kLzMRows - 2K rows and the 62 interior words
 // are exact and are the only ones stored.  Coins exactly as loz_sweep_kernel.
-template <int TM>
-__global__ void __launch_bounds__(32 * kLzMRows, 2) lz_multi_kernel(LzMCtx c) {
+template <int TM, int MINB = 2>
+__global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint4(*acs)[32] = reinterpret_cast<uint4(*)[32]>(dsm);
     uint2(*fs)[32] = reinterpret_cast<uint2(*)[32]>(dsm + sizeof(uint4) * kLzMRows * 32);
@@ -666,6 +667,13 @@ int lz_launch_multi(tsb_loz *h, int chain0, int n, uint64_t step_off, cudaStream
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // batches of several waves: the 3-blocks-per-SM build (register cap 40)
+    const bool dense = h->m_dense >= 0 ? h->m_dense == 1 : (int64_t)h->nmtiles * n > 4 * (int64_t)h->m_sms;
+    if (dense) {
+        if (h->tmode == 0) TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<0, 3>, c));
+        else TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<2, 3>, c));
+        return TSB_OK;
+    }
     if (h->tmode == 0) TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<0>, c));
     else TSB_CUDA(cudaLaunchKernelEx(&cfg, lz_multi_kernel<2>, c));
     return TSB_OK;
@@ -830,6 +838,11 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
         if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mt.size()))) != cudaSuccess)
             return bail(e, "tiles");
         if (!mt.empty()) cudaMemcpy(h->mtiles, mt.data(), sizeof(int2) * mt.size(), cudaMemcpyHostToDevice);
+        for (const void *fn : {(const void *)lz_multi_kernel<0, 3>, (const void *)lz_multi_kernel<2, 3>})
+            if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLzMSmem)) != cudaSuccess)
+                return bail(e, "smem attribute");
+        cudaDeviceGetAttribute(&h->m_sms, cudaDevAttrMultiProcessorCount, h->device);
+        if (const char *ev = getenv("TSB_LZ_DENSE")) h->m_dense = atoi(ev) ? 1 : 0;
         if ((e = cudaFuncSetAttribute(lz_multi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kLzMSmem)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(lz_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
