@@ -183,8 +183,8 @@ constexpr size_t sv_multi_smem() {
            + sizeof(uint16_t) * NW * (32 * WPL) * 16;   // per-warp job queues
 }
 
-template <int WPL, int NW>
-__global__ void __launch_bounds__(32 * NW) sv_multi_kernel(SvMCtx c) {
+template <int WPL, int NW, int MINB = 1>
+__global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
     constexpr int TW = 32 * WPL, TR = 2 * NW;
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t(*rows)[TW] = reinterpret_cast<uint32_t(*)[TW]>(dsm);
@@ -540,10 +540,20 @@ static int sv_launch_multi_t(const cudaLaunchConfig_t &cfg0, const SvMCtx &c, in
     constexpr size_t smem = sv_multi_smem<WPL, NW>();
     const size_t blocks = (size_t)cfg0.gridDim.x * cfg0.gridDim.y * cfg0.gridDim.z;
     const size_t use = blocks <= (size_t)sms ? std::max(smem, kSvSpreadSmem) : smem;
-    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
     cudaLaunchConfig_t cfg = cfg0;
     cfg.blockDim = dim3(32 * NW);
     cfg.dynamicSmemBytes = use;
+    static const int dense_env = [] {
+        const char *ev = getenv("TSB_SV_DENSE");  // 0 / 1: force the 1- / 2-blocks-per-SM build
+        return ev ? atoi(ev) : -1;
+    }();
+    const bool dense = NW == 16 && (dense_env >= 0 ? dense_env == 1 : blocks > 4 * (size_t)sms);
+    if (dense) {
+        TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
+        TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW, 2>, c));
+        return TSB_OK;
+    }
+    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
     TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW>, c));
     return TSB_OK;
 }
