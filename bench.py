@@ -467,7 +467,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (S // walk_len) * launches_per_walk(walk_len),
+            "gpu_launches": args.steps * (S // walk_len) * (launches_per_walk(walk_len)
+                                                           + (3 if strips and not args.host_exchange else 0)),  # + push/pull/epoch
         }
         print(json.dumps(line), flush=True)
     if world > 1:
