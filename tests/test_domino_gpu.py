@@ -365,9 +365,31 @@ def test_adaptive_dispatch_order_is_exact(monkeypatch, adapt):
     equal the oracle, with the adaptive order on and off."""
     monkeypatch.setenv("TSB_DOM_ADAPT", adapt)
     monkeypatch.setenv("TSB_DOM_RESIDENT", "0")
+    monkeypatch.setenv("TSB_DOM_WPL", "2")  # the adaptive order serves the 2-word kernel
     d = ts.Domain.aztec(300)
     plan = ts.SweepPlan(d)
     t_max, t_min = ts.extremal_tilings(d)
     start = t_max.states[None]
     out = ts.random_walk_batch(start, [0x5EED], 1000, plan)
     assert np.array_equal(out, oracle.domino_walk(start, [0x5EED], plan.p_up, 1000))
+
+
+@pytest.mark.parametrize("weights", ["edge", "volume_site"])
+def test_adaptive_order_with_per_site_thresholds(monkeypatch, weights):
+    """Per-site threshold grids (EdgeWeights; VolumeWeights with face
+    overrides) through whole-domain graph replays with the adaptive tile
+    order, on a batch of 3 chains (2-word tiles forced: the adaptive order
+    serves the one-block-per-tile 2-word kernel)."""
+    monkeypatch.setenv("TSB_DOM_RESIDENT", "0")
+    monkeypatch.setenv("TSB_DOM_WPL", "2")
+    d = ts.Domain.aztec(60)
+    if weights == "edge":
+        w = ts.EdgeWeights(1.0, {((60, 60), (60, 61)): 3.0, ((30, 50), (31, 50)): 0.25})
+    else:
+        w = ts.VolumeWeights(0.95, {(60, 60): 3.0, (40, 70): 0.4})
+    plan = ts.SweepPlan(d, w)
+    t_max, t_min = ts.extremal_tilings(d)
+    start = np.stack([t_max.states, t_min.states, t_max.states])
+    seeds = np.array([1, 2, 3], dtype=np.uint64)
+    out = ts.random_walk_batch(start, seeds, 530, plan)
+    assert np.array_equal(out, oracle.domino_walk(start, seeds, plan.p_up, 530))
