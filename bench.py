@@ -74,13 +74,79 @@ def workload(order: int):
 
     d = ts.Domain.aztec(order)
     t_max, _ = aztec_extremal_states(order)
-    mask = d.vertex_mask
-    black, cols = 0, np.arange(d.n + 1)
-    for r0 in range(0, d.n + 1, 2048):  # row blocks: no n^2 integer temporaries
-        rows = np.arange(r0, min(d.n + 1, r0 + 2048))
-        black += int((mask[r0:r0 + 2048] & (((rows[:, None] + cols[None, :]) & 1) == 0)).sum())
-    counts = (black, int(mask.sum()) - black)  # BLACK, WHITE
-    return d, t_max, counts
+    return d, t_max, aztec_counts(order)
+
+
+# ---- package-free host side of the workload (the reference arm and the CPU
+# baseline never import paper_1804_07250_b200 or load libtsb.so) -------------
+_M64 = (1 << 64) - 1
+
+
+def _mix(z: int) -> int:
+    """splitmix64 finaliser (reference rng.py:34-39)."""
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _color_at(seed: int, step: int) -> int:
+    """Domino colour coin (sweeps.py:266-269: WHITE iff u >= 0.5 = bit 63 of
+    the global draw; global key rng.py:101-103)."""
+    g = 0x9E3779B97F4A7C15
+    gkey = _mix(_mix((seed & _M64) ^ 0x6A09E667F3BCC909) + ((1 << 48) + 1) * g)
+    return _mix(gkey + (step + 1) * g) >> 63
+
+
+def _face_range(order: int, i: int):
+    """Columns [a, b] of face row i of the Aztec diamond (Domain.aztec,
+    lattice.py:156-162: |r+0.5-order| + |c+0.5-order| <= order)."""
+    di = abs(2 * i + 1 - 2 * order)  # 2 * |i + 0.5 - order|
+    return (di - 1) // 2, (4 * order - di - 1) // 2
+
+
+def aztec_counts(order: int):
+    """(BLACK, WHITE) in-domain vertices (vertex_mask: vertices touching a
+    face), row by row without V x V temporaries."""
+    n = 2 * order
+    black = total = 0
+    for r in range(n + 1):
+        rows = [i for i in (r - 1, r) if 0 <= i < n]
+        a = min(_face_range(order, i)[0] for i in rows)
+        b = max(_face_range(order, i)[1] for i in rows) + 1
+        cnt = b - a + 1
+        first_even = (a + r) % 2 == 0
+        black += (cnt + 1) // 2 if first_even else cnt // 2
+        total += cnt
+    return black, total - black
+
+
+def aztec_tmax_host(order: int) -> np.ndarray:
+    """Closed-form T_max: all-horizontal bricks for
+    even order, all-vertical for odd, each row (column) paired from its first
+    face; the tilestate bit of a brick's interior edge (lattice.py:51-53)."""
+    n = 2 * order
+    s = np.zeros((n + 1, n + 1), dtype=np.uint8)
+    for i in range(n):
+        a, b = _face_range(order, i)
+        x = np.arange(a + 1, b + 1, 2)
+        s[i, x] |= 2
+        s[i + 1, x] |= 1
+    if order % 2 == 0:
+        return s
+    t = np.ascontiguousarray(s.T)
+    return (((t & 1) << 2) | ((t & 2) << 2)).astype(np.uint8)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 MK = 2            # sweeps per domino_multi_kernel launch (kMK in csrc/domino.cu)
@@ -103,9 +169,7 @@ def launches_per_walk(n: int) -> int:
 
 
 def attempts_for(seed: int, step0: int, n: int, counts) -> int:
-    from paper_1804_07250_b200 import rng
-
-    return sum(counts[rng.color_at(seed, s)] for s in range(step0, step0 + n))
+    return sum(counts[_color_at(seed, s)] for s in range(step0, step0 + n))
 
 
 def traffic(kernel: str):
@@ -184,11 +248,10 @@ def cpu_baseline(order: int, budget_s: float = 12.0):
     """The reference algorithm's CPU path (oracle/ C port of _kernels.py
     domino_walk, pthread row bands over all host threads) on a bounded sample."""
     import oracle
-    from paper_1804_07250_b200.lattice import aztec_extremal_states
 
-    d, t_max, counts = workload(order)
+    t_max, counts = aztec_tmax_host(order), aztec_counts(order)
     threads = os.cpu_count() or 1
-    p_up = np.full((d.n + 1, d.n + 1), 0.5)
+    p_up = np.full(t_max.shape, 0.5)
     t0 = time.perf_counter()
     s = oracle.domino_walk(t_max[None], [SEED], p_up, 1, threads=threads)
     one = time.perf_counter() - t0
@@ -197,7 +260,7 @@ def cpu_baseline(order: int, budget_s: float = 12.0):
     oracle.domino_walk(s, [SEED], p_up, n, step0=1, threads=threads)
     dt = time.perf_counter() - t0
     att = attempts_for(SEED, 1, n, counts)
-    return {"value": att / dt, "unit": UNIT, "cores": threads, "kind": "port",
+    return {"value": att / dt, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_model(),
             "sample": f"aztec order {order} from T_max, sweeps 1..{n} of seed 0x5EED ({dt:.1f} s)"}
 
 
@@ -205,11 +268,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
+    import oracle  # the C port of the reference's CPU path; nothing of the product is imported
 
-    d, t_max, counts = workload(args.order)
+    t_max, counts = aztec_tmax_host(args.order), aztec_counts(args.order)
     threads = os.cpu_count() or 1
-    p_up = np.full((d.n + 1, d.n + 1), 0.5)
+    p_up = np.full(t_max.shape, 0.5)
     s = t_max[None].copy()
     t0 = time.perf_counter()
     s = oracle.domino_walk(s, [SEED], p_up, 1, threads=threads)
@@ -236,25 +299,54 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": {"workload": f"aztec{args.order}_uniform_from_Tmax",
                                         "sweeps_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: start N ranks of
+    this script the way the driver does (one process per GPU, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and world_env is None:
+        sys.exit(relaunch_under_torchrun(args))
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    # more ranks than visible GPUs (a functional check on a 1-GPU box): ranks
+    # share devices round-robin and the host collectives go through gloo
+    # (NCCL refuses two ranks on one device); timings are then not scaling data
+    shared_gpu = world > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if shared_gpu else "cuda"
 
     import paper_1804_07250_b200 as ts
     from paper_1804_07250_b200 import _native, rng
@@ -324,8 +416,8 @@ def main():
         dist.barrier()
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     att = attempts_for(seed, first, step - first, counts)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    a = torch.tensor([float(att)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
+    a = torch.tensor([float(att)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if not strips:  # replicas: every rank ran its own chain
@@ -360,7 +452,7 @@ def main():
             step += S
             host.copy_(row_engine.get_rows(walker.lo, rows), non_blocking=True)  # the step's result
             torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e_att = attempts_for(seed, step - args.steps * S, args.steps * S, counts)
         e2e = {"value": e2e_att / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": 8,
@@ -427,8 +519,8 @@ def main():
         cur = ts.random_walk(cur, rng.derive_seed(seed, 99, 7), S, plan)
         dt_plain = time.perf_counter() - t1
         att_plain = attempts_for(rng.derive_seed(seed, 99, 7), 0, S, counts)
-        e2e_v = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        e2e_a = torch.tensor([float(e2e_att)], dtype=torch.float64, device="cuda")
+        e2e_v = torch.tensor([dt], dtype=torch.float64, device=red_dev)
+        e2e_a = torch.tensor([float(e2e_att)], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(e2e_v, op=dist.ReduceOp.MAX)
             dist.all_reduce(e2e_a, op=dist.ReduceOp.SUM)
@@ -448,6 +540,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            **({"shared_gpu": f"{world} ranks on {ndev} visible GPU(s): functional run, not scaling data"}
+               if shared_gpu else {}),
             "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic: Aztec diamond from the closed-form T_max, uniform weights",
             "config": {"workload": f"aztec{args.order}_uniform_from_Tmax", "order": args.order,
