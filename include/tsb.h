@@ -52,6 +52,12 @@ int tsb_abi_version(void);
  * (faces connected <=> 1 component; no hole <=> the complement padded by one
  * ring of cells is 1 component) without the reference's Python DFS. */
 int tsb_grid_components(int device, const uint8_t *grid, int rows, int cols, int64_t *ncomp);
+/* TriDomain checks (lozenge.py:185-210) on the device: number of
+ * edge-connected components of the up/down triangles ((sx, sy) uint8 grids;
+ * up(x,y) touches down(x,y), down(x-1,y), down(x,y-1)) and the Euler
+ * characteristic V - E + F (simply connected <=> 1). */
+int tsb_tri_check(int device, const uint8_t *up, const uint8_t *down, int sx, int sy, int64_t *ncomp,
+                  int64_t *euler);
 int tsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor, int64_t *l2_bytes);
 
 /* ------------------------------------------------------------------- RNG */
@@ -153,6 +159,13 @@ int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, 
  * outside the domain stay 0.  density_map = acc / (#states added). */
 int tsb_domino_orientation_add(tsb_domino *h, int chain0, int n, uint32_t *acc_dev);
 
+/* Heights of chains [chain0, chain0+n) (height_function, lattice.py:537-551,
+ * reference vertex (ref_r, ref_c)) added to the caller's device int64
+ * accumulator acc_dev (side^2, row-major; 0 outside vertex_mask): the mean
+ * height function = acc / (#states added).  TSB_E_INCONSISTENT as
+ * tsb_domino_heights. */
+int tsb_domino_height_sum_add(tsb_domino *h, int chain0, int n, int ref_r, int ref_c, long long *acc_dev);
+
 /* Sample-archive record of chain `chain` (stats.py:146-153
  * _serialize_state): the tilestates joined by single spaces in decimal, as one
  * line without the newline, formatted on the device.  With out == NULL or
@@ -246,6 +259,9 @@ int tsb_loz_sweep(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t
 int tsb_loz_sync(tsb_loz *h);
 /* loz_heights (lozenge.py:414-447): int32 (sx+1, sy+1), 0 outside the mask. */
 int tsb_loz_heights(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *out);
+/* loz_heights of chains [chain0, chain0+n) added to a device int64
+ * accumulator ((sx+1) x (sy+1)): mean height function = acc / #states. */
+int tsb_loz_height_sum_add(tsb_loz *h, int chain0, int n, int ref_x, int ref_y, long long *acc_dev);
 /* loz_extremal (lozenge.py:762-775) into chains chain_max / chain_min;
  * TSB_E_UNTILEABLE when the domain has no tiling. */
 int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int ref_y);

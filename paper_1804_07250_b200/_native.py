@@ -79,6 +79,7 @@ _SIGS = {
     "tsb_abi_version": (_i, []),
     "tsb_device_info": (_i, [_i, _vp, _vp, _vp, _vp]),
     "tsb_grid_components": (_i, [_i, _vp, _i, _i, _vp]),
+    "tsb_tri_check": (_i, [_i, _vp, _vp, _i, _i, _vp, _vp]),
     "tsb_uniform_grid": (_i, [_i, _u64, _i, _i, _u64, _i, _vp]),
     "tsb_domino_create": (_i, [_i, _i, _i, _vp, _vp]),
     "tsb_domino_destroy": (_i, [_vp]),
@@ -99,6 +100,7 @@ _SIGS = {
     "tsb_domino_extremal": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_domino_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_orientation_add": (_i, [_vp, _i, _i, _vp]),
+    "tsb_domino_height_sum_add": (_i, [_vp, _i, _i, _i, _i, _vp]),
     "tsb_domino_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
     "tsb_sv_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
     "tsb_loz_serialize": (_i, [_vp, _i, _vp, ctypes.c_size_t, _vp]),
@@ -137,6 +139,7 @@ _SIGS = {
     "tsb_loz_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
     "tsb_loz_sync": (_i, [_vp]),
     "tsb_loz_heights": (_i, [_vp, _i, _i, _i, _vp]),
+    "tsb_loz_height_sum_add": (_i, [_vp, _i, _i, _i, _i, _vp]),
     "tsb_loz_extremal": (_i, [_vp, _i, _i, _i, _i]),
     "tsb_loz_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_loz_replicate": (_i, [_vp, _i, _i, _i, _i]),

@@ -1157,6 +1157,10 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->dom);
     cudaFree(h->fbits);
     cudaFree(h->range);
+    cudaFree(h->hx_h);
+    cudaFree(h->hx_flags);
+    cudaFree(h->hx_rows);
+    cudaFree(h->hx_off);
     cudaFree(h->tiles);
     cudaFree(h->mtiles);
     cudaFree(h->m_order);

@@ -50,6 +50,14 @@ struct tsb_domino {
     int g_chain0 = -1, g_n = -1, g_cur = -1, g_tmode = -1;
     uint64_t g_t0 = 0, g_t1 = 0;
     int g_win0 = -1, g_winn = -1, g_winm = -1;
+    // height export scratch (heights.cu), allocated on first use and owned by
+    // the handle: no cudaMalloc / cudaFree per call
+    int *hx_h = nullptr;        // side^2 int32: working heights / per-row prefix sums
+    int *hx_flags = nullptr;    // 4 device flags
+    int4 *hx_rows = nullptr;    // per row {first, last in-domain vertex, link column, ok}
+    int *hx_off = nullptr;      // per row height offsets
+    int hx_scan = -1;           // -1 not classified, 0 relaxation only, 1 row scan
+    int hx_r0 = 0, hx_r1 = -1;  // non-empty vertex rows
     struct tsb_strip *strip = nullptr;  // device-driven strip exchange (strips.cu), if set up
     // work captured at the end of every graph replay (strip exchange), null: none
     int (*graph_tail)(tsb_domino *, cudaStream_t) = nullptr;

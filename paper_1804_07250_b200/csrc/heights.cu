@@ -16,6 +16,10 @@
 // ((r+c) odd) on the left, +1 uncrossed / -3 crossed; mirrored otherwise.
 // For the edge entering vertex (r,c) from its vertical neighbours the left
 // face is dark iff (r+c) is even; from its horizontal neighbours iff odd.
+#include <climits>
+#include <cstdlib>
+#include <vector>
+
 #include "domino.cuh"
 
 namespace tsb {
@@ -218,6 +222,246 @@ int relax(tsb_domino *h, int *dh, int ref, const uint2 *st, int *dflags, bool *o
     return TSB_OK;
 }
 
+// ---------------------------------------------------------------- row scan
+// Fast exact height export for domains whose vertex rows are intervals joined
+// by horizontal domain edges, with consecutive rows linked by a vertical
+// domain edge (every convex-row domain: Aztec diamonds, rectangles, ...).
+// A consistent state's heights are path-independent, so
+//   h(r, c) = off[r] + local(r, c),  local(r, c) = sum of the horizontal steps
+//   from the row's first vertex, off[r] chained through one vertical link
+// per row and shifted so h(reference vertex) = 0.  Every vertical domain edge
+// is then checked against its step (lattice.py:554-580
+// _check_height_consistency), so inconsistent states still raise.  Three
+// passes over the int32 grid instead of ~2·side/31 relaxation rounds.
+
+// step of edge a -> b whose "left face dark" flag is `dark` (lattice.py:17-20)
+__device__ __forceinline__ int hstep(bool crossed, bool dark) {
+    return dark ? (crossed ? -3 : 1) : (crossed ? 3 : -1);
+}
+
+// vertex (r, c) of word w lies in vertex_mask iff one of its edges exists
+__device__ __forceinline__ uint32_t in_mask(const uint4 *dom, int r, int w, int pitch) {
+    const uint4 d = dom[(size_t)r * pitch + w];
+    uint32_t m = d.z | d.w | (d.w << 1);
+    if (w > 0) m |= dom[(size_t)r * pitch + w - 1].w >> 31;
+    if (r > 0) m |= dom[(size_t)(r - 1) * pitch + w].z;
+    return m;
+}
+
+// Row classification, once per handle: {first, last} in-domain vertex,
+// link = first column with a vertical domain edge to the row above (-1:
+// none), ok = every horizontal edge between first and last exists.
+__global__ void __launch_bounds__(256) hx_rows_kernel(const uint4 *dom, int side, int pitch, int W, int4 *rows) {
+    __shared__ int sh[8];
+    const int r = blockIdx.x;
+    int a = INT_MAX, b = -1, link = INT_MAX;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const uint32_t m = in_mask(dom, r, w, pitch);
+        if (m) {
+            a = min(a, w * 32 + __ffs(m) - 1);
+            b = max(b, w * 32 + 31 - __clz(m));
+        }
+        if (r > 0) {
+            const uint32_t up = dom[(size_t)(r - 1) * pitch + w].z;
+            if (up) link = min(link, w * 32 + __ffs(up) - 1);
+        }
+    }
+    a = block_reduce(a, [](int x, int y) { return min(x, y); }, sh);
+    b = block_reduce(b, [](int x, int y) { return max(x, y); }, sh);
+    link = block_reduce(link, [](int x, int y) { return min(x, y); }, sh);
+    int missing = 0;
+    if (a <= b) {
+        for (int w = (a >> 5) + threadIdx.x; w <= ((b - 1) >> 5) && b > a; w += blockDim.x) {
+            uint32_t e = 0xffffffffu;  // edges c in [a, b)
+            if (w == (a >> 5)) e &= 0xffffffffu << (a & 31);
+            if (w == ((b - 1) >> 5)) e &= 0xffffffffu >> (31 - ((b - 1) & 31));
+            missing += __popc(e & ~dom[(size_t)r * pitch + w].w);
+        }
+    }
+    missing = block_reduce(missing, [](int x, int y) { return x + y; }, sh);
+    if (threadIdx.x == 0) rows[r] = make_int4(a, b, link == INT_MAX ? -1 : link, missing == 0);
+}
+
+// local(r, c) for c in [first, last] of row r: one block per row, thread t
+// owns consecutive words; word sums by popcount, block exclusive scan, then
+// the per-vertex prefix within the word.
+__global__ void __launch_bounds__(256) hx_local_kernel(const uint2 *st, int pitch, int side, int r0,
+                                                      const int4 *rows, int *loc) {
+    __shared__ int sh[8];
+    const int r = r0 + blockIdx.x;
+    const int4 ri = rows[r];
+    const int a = ri.x, b = ri.y;
+    if (a > b) return;
+    const int w0 = a >> 5, w1 = b >> 5, nw = w1 - w0 + 1;
+    const int per = (nw + blockDim.x - 1) / blockDim.x;
+    const int wa = w0 + threadIdx.x * per, wb = min(w1, wa + per - 1);
+    const uint32_t D = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // dark: (r + c) even
+    const uint2 *row = st + (size_t)(r + 1) * pitch;
+    int sum = 0;
+    for (int w = wa; w <= wb; ++w) {
+        uint32_t e = 0xffffffffu;  // edges c in [a, b)
+        if (w == w0) e &= 0xffffffffu << (a & 31);
+        if (w == w1) e = (b & 31) ? (e & (0xffffffffu >> (32 - (b & 31)))) : 0u;
+        const uint32_t x = row[w].y;
+        sum += __popc(e & D & ~x) - 3 * __popc(e & D & x) - __popc(e & ~D & ~x) + 3 * __popc(e & ~D & x);
+    }
+    int acc = block_exclusive_sum(sum, sh);
+    int *out = loc + (size_t)r * side;
+    for (int w = wa; w <= wb; ++w) {
+        const uint32_t x = row[w].y;
+        const int cb = max(a, w * 32), ce = min(b, w * 32 + 31);
+        for (int c = cb; c <= ce; ++c) {
+            out[c] = acc;
+            acc += hstep((x >> (c & 31)) & 1u, ((r + c) & 1) == 0);
+        }
+    }
+}
+
+// Row offsets: delta[r] through the vertical link edge, block scan over the
+// rows r0..r1 (one block, 1024 threads, consecutive rows per thread), then
+// the shift that puts the reference vertex at 0.  flags[0]: a row without a
+// link (cannot happen for a classified domain).
+__global__ void __launch_bounds__(1024) hx_offsets_kernel(const uint2 *st, int pitch, int side, int r0, int r1,
+                                                         const int4 *rows, const int *loc, int *off, int ref_r,
+                                                         int ref_c) {
+    __shared__ int sh[32];
+    const int nr = r1 - r0 + 1;
+    const int per = (nr + blockDim.x - 1) / blockDim.x;
+    const int ra = r0 + threadIdx.x * per, rb = min(r1, ra + per - 1);
+    int sum = 0;
+    for (int r = ra; r <= rb; ++r) {
+        int d = 0;
+        if (r > r0) {
+            const int c = rows[r].z;
+            const bool x = (st[(size_t)r * pitch + (c >> 5)].x >> (c & 31)) & 1u;  // V(r-1, c)
+            d = loc[(size_t)(r - 1) * side + c] + hstep(x, ((r + c) & 1) == 0) - loc[(size_t)r * side + c];
+        }
+        sum += d;
+        off[r] = sum;  // partial within the thread's run
+    }
+    const int excl = block_exclusive_sum(sum, sh);
+    for (int r = ra; r <= rb; ++r) off[r] += excl;
+    __syncthreads();
+    const int shift = off[ref_r] + loc[(size_t)ref_r * side + ref_c];
+    __syncthreads();
+    for (int r = ra; r <= rb; ++r) off[r] -= shift;
+}
+
+// h = off[r] + local inside vertex_mask, 0 outside; every vertical domain
+// edge checked (flags[0] on a violation).  SUM: add into an int64
+// accumulator instead of writing the grid.
+template <bool SUM>
+__global__ void __launch_bounds__(256) hx_finish_kernel(const uint2 *st, const uint4 *dom, int pitch, int side, int r0,
+                                                       int r1, const int *loc, const int *off, int32_t *out,
+                                                       long long *acc, int *flags) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (c >= side) return;
+    const int w = c >> 5;
+    const bool in = r >= r0 && r <= r1 && ((in_mask(dom, r, w, pitch) >> (c & 31)) & 1u);
+    int v = 0;
+    if (in) {
+        v = off[r] + loc[(size_t)r * side + c];
+        if (r > 0 && ((dom[(size_t)(r - 1) * pitch + w].z >> (c & 31)) & 1u)) {
+            const bool x = (st[(size_t)r * pitch + w].x >> (c & 31)) & 1u;
+            const int up = off[r - 1] + loc[(size_t)(r - 1) * side + c];
+            if (v - up != hstep(x, ((r + c) & 1) == 0)) atomicExch(flags, 1);
+        }
+    }
+    if (SUM) acc[(size_t)r * side + c] += v;
+    else out[(size_t)r * side + c] = v;
+}
+
+__global__ void add_heights_kernel(const int32_t *h, size_t n, long long *acc) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) acc[i] += h[i];
+}
+
+int hx_scratch(tsb_domino *h) {
+    if (h->hx_h) return TSB_OK;
+    const size_t nv = (size_t)h->side * h->side;
+    TSB_CUDA(cudaMalloc(&h->hx_h, nv * sizeof(int)));
+    TSB_CUDA(cudaMalloc(&h->hx_flags, 4 * sizeof(int)));
+    TSB_CUDA(cudaMalloc(&h->hx_rows, h->side * sizeof(int4)));
+    TSB_CUDA(cudaMalloc(&h->hx_off, h->side * sizeof(int)));
+    return TSB_OK;
+}
+
+// classify the domain once: row scan when every non-empty row is an interval
+// of horizontal domain edges and every row after the first has a link
+int hx_classify(tsb_domino *h) {
+    if (h->hx_scan >= 0) return TSB_OK;
+    int rc = hx_scratch(h);
+    if (rc) return rc;
+    hx_rows_kernel<<<h->side, 256, 0, h->stream>>>(h->dom, h->side, h->pitch, h->W, h->hx_rows);
+    TSB_CUDA(cudaGetLastError());
+    std::vector<int4> rows(h->side);
+    TSB_CUDA(cudaMemcpyAsync(rows.data(), h->hx_rows, sizeof(int4) * h->side, cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    int r0 = -1, r1 = -1;
+    bool ok = true;
+    for (int r = 0; r < h->side; ++r) {
+        if (rows[r].x > rows[r].y) continue;
+        if (r0 < 0) r0 = r;
+        else if (r1 != r - 1 || rows[r].z < 0) ok = false;  // a gap row, or no vertical link
+        if (!rows[r].w) ok = false;
+        r1 = r;
+    }
+    h->hx_r0 = r0 < 0 ? 0 : r0;
+    h->hx_r1 = r0 < 0 ? -1 : r1;
+    h->hx_scan = (ok && r0 >= 0) ? 1 : 0;
+    const char *env = getenv("TSB_HEIGHTS_RELAX");  // test knob: force the relaxation path
+    if (env && env[0] == '1') h->hx_scan = 0;
+    return TSB_OK;
+}
+
+// Heights of one chain into dout (device, side^2 int32) or added to acc.
+// Returns TSB_E_INCONSISTENT for an inconsistent state.
+int domino_heights_dev(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *dout, long long *acc) {
+    int rc = hx_classify(h);
+    if (rc) return rc;
+    const size_t nv = (size_t)h->side * h->side;
+    const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride + kStatePad;
+    int hf[2] = {0, 0};
+    const int ref = ref_r * h->side + ref_c;
+    const dim3 fgrid((h->side + 255) / 256, h->side);
+    if (h->hx_scan == 1 && ref_r >= h->hx_r0 && ref_r <= h->hx_r1) {
+        TSB_CUDA(cudaMemsetAsync(h->hx_flags, 0, 2 * sizeof(int), h->stream));
+        hx_local_kernel<<<h->hx_r1 - h->hx_r0 + 1, 256, 0, h->stream>>>(st, h->pitch, h->side, h->hx_r0, h->hx_rows,
+                                                                        h->hx_h);
+        hx_offsets_kernel<<<1, 1024, 0, h->stream>>>(st, h->pitch, h->side, h->hx_r0, h->hx_r1, h->hx_rows, h->hx_h,
+                                                     h->hx_off, ref_r, ref_c);
+        if (acc)
+            hx_finish_kernel<true><<<fgrid, 256, 0, h->stream>>>(st, h->dom, h->pitch, h->side, h->hx_r0, h->hx_r1,
+                                                                 h->hx_h, h->hx_off, nullptr, acc, h->hx_flags);
+        else
+            hx_finish_kernel<false><<<fgrid, 256, 0, h->stream>>>(st, h->dom, h->pitch, h->side, h->hx_r0, h->hx_r1,
+                                                                  h->hx_h, h->hx_off, dout, nullptr, h->hx_flags);
+        TSB_CUDA(cudaGetLastError());
+        TSB_CUDA(cudaMemcpyAsync(hf, h->hx_flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        TSB_CUDA(cudaStreamSynchronize(h->stream));
+        if (hf[0]) return fail(TSB_E_INCONSISTENT, "height propagation is cyclically inconsistent");
+        return TSB_OK;
+    }
+    bool overflow = false;
+    if ((rc = relax<0>(h, h->hx_h, ref, st, h->hx_flags, &overflow))) return rc;
+    if (overflow) return fail(TSB_E_INCONSISTENT, "height propagation is cyclically inconsistent");
+    int32_t *o = dout;
+    if (acc) {
+        if ((rc = ensure_bytes(h, nv * sizeof(int32_t)))) return rc;
+        o = reinterpret_cast<int32_t *>(h->bytes);
+    }
+    TSB_CUDA(cudaMemsetAsync(h->hx_flags, 0, sizeof(int), h->stream));
+    finish_heights_kernel<<<dim3((h->side + 127) / 128, h->side), 128, 0, h->stream>>>(
+        h->hx_h, h->dom, h->side, h->pitch, o, kInf, h->hx_flags);
+    if (acc) add_heights_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, h->stream>>>(o, nv, acc);
+    TSB_CUDA(cudaGetLastError());
+    TSB_CUDA(cudaMemcpyAsync(hf, h->hx_flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (hf[0]) return fail(TSB_E_INCONSISTENT, "height propagation is cyclically inconsistent");
+    return TSB_OK;
+}
+
 }  // namespace tsb
 
 using namespace tsb;
@@ -231,30 +475,24 @@ int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *
         return fail(TSB_E_VALUE, "reference vertex outside the grid");
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t nv = (size_t)h->side * h->side;
-    int *dh = nullptr, *dflags = nullptr;
-    int32_t *dout = nullptr;
-    TSB_CUDA(cudaMalloc(&dh, nv * sizeof(int)));
-    TSB_CUDA(cudaMalloc(&dout, nv * sizeof(int32_t)));
-    TSB_CUDA(cudaMalloc(&dflags, 2 * sizeof(int)));
-    bool overflow = false;
-    const uint2 *st = h->buf[h->cur] + (size_t)chain * h->chain_stride + kStatePad;
-    int rc = relax<0>(h, dh, ref_r * h->side + ref_c, st, dflags, &overflow);
-    int hf = 0;
-    if (!rc && !overflow) {
-        cudaMemsetAsync(dflags, 0, sizeof(int), h->stream);
-        finish_heights_kernel<<<dim3((h->side + 127) / 128, h->side), 128, 0, h->stream>>>(
-            dh, h->dom, h->side, h->pitch, dout, kInf, dflags);
-        cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
-        cudaMemcpyAsync(&hf, dflags, sizeof(int), cudaMemcpyDeviceToHost, h->stream);
-        cudaError_t e = cudaStreamSynchronize(h->stream);
-        if (e != cudaSuccess) rc = cuda_fail(e, "heights");
-    }
-    cudaFree(dh);
-    cudaFree(dout);
-    cudaFree(dflags);
+    int rc = ensure_bytes(h, nv * sizeof(int32_t));  // handle staging: no allocation per call
     if (rc) return rc;
-    if (overflow || hf) return fail(TSB_E_INCONSISTENT, "height propagation is cyclically inconsistent");
+    int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
+    if ((rc = domino_heights_dev(h, chain, ref_r, ref_c, dout, nullptr))) return rc;
+    TSB_CUDA(cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
     return TSB_OK;
+}
+
+int tsb_domino_height_sum_add(tsb_domino *h, int chain0, int n, int ref_r, int ref_c, long long *acc_dev) {
+    int rc = check_range(h, chain0, n);
+    if (rc || n == 0) return rc;
+    if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");
+    if (ref_r < 0 || ref_c < 0 || ref_r >= h->side || ref_c >= h->side)
+        return fail(TSB_E_VALUE, "reference vertex outside the grid");
+    TSB_CUDA(cudaSetDevice(h->device));
+    for (int k = 0; k < n && !rc; ++k) rc = domino_heights_dev(h, chain0 + k, ref_r, ref_c, nullptr, acc_dev);
+    return rc;
 }
 
 // Thurston extremal tilings into chains `chain_max` / `chain_min`.
@@ -266,12 +504,11 @@ int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, 
         return fail(TSB_E_VALUE, "chain out of range");
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t nv = (size_t)h->side * h->side;
-    int *dh = nullptr, *dflags = nullptr;
-    int32_t *dout = nullptr;
-    TSB_CUDA(cudaMalloc(&dh, nv * sizeof(int)));
-    TSB_CUDA(cudaMalloc(&dout, nv * sizeof(int32_t)));
-    TSB_CUDA(cudaMalloc(&dflags, 2 * sizeof(int)));
-    int rc = TSB_OK;
+    int rc = hx_scratch(h);
+    if (!rc) rc = ensure_bytes(h, nv * sizeof(int32_t));
+    if (rc) return rc;
+    int *dh = h->hx_h, *dflags = h->hx_flags;
+    int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
     bool untileable = false;
     for (int pass = 0; pass < 2 && !rc && !untileable; ++pass) {
         bool overflow = false;
@@ -292,9 +529,6 @@ int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, 
         if (e != cudaSuccess) { rc = cuda_fail(e, "extremal"); break; }
         if (hf[0] || hf[1]) untileable = true;
     }
-    cudaFree(dh);
-    cudaFree(dout);
-    cudaFree(dflags);
     if (rc) return rc;
     if (untileable) return fail(TSB_E_UNTILEABLE, "domain is not tileable");
     return TSB_OK;

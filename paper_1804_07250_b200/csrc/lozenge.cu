@@ -63,6 +63,10 @@ struct tsb_loz {
     int2 *mtiles = nullptr;  // tiles of the temporally blocked kernel (m_out-row bands)
     int nmtiles = 0;
     int m_K = 4, m_out = 8;
+    // height export scratch, allocated on first use (no cudaMalloc per call)
+    int *hx_h = nullptr, *hx_flags = nullptr, *hx_off = nullptr;
+    int4 *hx_rows = nullptr;
+    int hx_scan = -1, hx_r0 = 0, hx_r1 = -1;  // row-scan classification (-1: not yet)
 };
 
 namespace tsb {
@@ -748,6 +752,238 @@ int lz_relax(tsb_loz *h, int *dh, size_t ref, const uint32_t *st, int *dflags, b
     return TSB_OK;
 }
 
+// ------------------------------------------------------------ row-scan heights
+// Exact loz_heights (lozenge.py:414-447) for domains whose vertex rows x are
+// intervals of existing b-edges (direction d1, step +2 crossed / -1 not,
+// _STEPS lozenge.py:47) with consecutive rows linked by an a-edge (d0,
+// -2 / +1): h(x, y) = off[x] + local(x, y), then every a- and c-edge is
+// checked against its step, so inconsistent states still raise.  The same
+// construction as the domino row scan (heights.cu).
+
+__device__ __forceinline__ uint32_t lz_word(const uint32_t *p, int pitch, int x, int w) {
+    return p[(size_t)x * pitch + w];
+}
+
+// vertex_mask word: any of the six incident edges exists (lz_finish)
+__device__ __forceinline__ uint32_t lz_in_mask(const uint32_t *dom, int X, int W, int pitch, int x, int w) {
+    const size_t dp = (size_t)X * pitch;
+    const uint32_t *exA = dom + 3 * dp, *exB = dom + 4 * dp, *exC = dom + 5 * dp;
+    uint32_t m = lz_word(exA, pitch, x, w) | lz_word(exB, pitch, x, w) | lz_word(exC, pitch, x, w);
+    m |= lz_word(exB, pitch, x, w) << 1;
+    if (w > 0) m |= lz_word(exB, pitch, x, w - 1) >> 31;
+    if (x > 0) {
+        m |= lz_word(exA, pitch, x - 1, w) | (lz_word(exC, pitch, x - 1, w) >> 1);
+        if (w + 1 < W) m |= lz_word(exC, pitch, x - 1, w + 1) << 31;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(256) lz_hx_rows_kernel(const uint32_t *dom, int X, int W, int pitch, int4 *rows) {
+    __shared__ int sh[8];
+    const int x = blockIdx.x;
+    const size_t dp = (size_t)X * pitch;
+    const uint32_t *exA = dom + 3 * dp, *exB = dom + 4 * dp;
+    int a = INT_MAX, b = -1, link = INT_MAX;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const uint32_t m = lz_in_mask(dom, X, W, pitch, x, w);
+        if (m) {
+            a = min(a, w * 32 + __ffs(m) - 1);
+            b = max(b, w * 32 + 31 - __clz(m));
+        }
+        if (x > 0) {
+            const uint32_t up = lz_word(exA, pitch, x - 1, w);
+            if (up) link = min(link, w * 32 + __ffs(up) - 1);
+        }
+    }
+    a = block_reduce(a, [](int p, int q) { return min(p, q); }, sh);
+    b = block_reduce(b, [](int p, int q) { return max(p, q); }, sh);
+    link = block_reduce(link, [](int p, int q) { return min(p, q); }, sh);
+    int missing = 0;
+    if (a < b) {
+        for (int w = (a >> 5) + threadIdx.x; w <= ((b - 1) >> 5); w += blockDim.x) {
+            uint32_t e = 0xffffffffu;  // b-edges y in [a, b)
+            if (w == (a >> 5)) e &= 0xffffffffu << (a & 31);
+            if (w == ((b - 1) >> 5)) e &= 0xffffffffu >> (31 - ((b - 1) & 31));
+            missing += __popc(e & ~lz_word(exB, pitch, x, w));
+        }
+    }
+    missing = block_reduce(missing, [](int p, int q) { return p + q; }, sh);
+    if (threadIdx.x == 0) rows[x] = make_int4(a, b, link == INT_MAX ? -1 : link, missing == 0);
+}
+
+__global__ void __launch_bounds__(256) lz_hx_local_kernel(const uint32_t *st, size_t plane, int pitch, int Y, int r0,
+                                                         const int4 *rows, int *loc) {
+    __shared__ int sh[8];
+    const int x = r0 + blockIdx.x;
+    const int4 ri = rows[x];
+    const int a = ri.x, b = ri.y;
+    if (a > b) return;
+    const int w0 = a >> 5, w1 = b >> 5, nw = w1 - w0 + 1;
+    const int per = (nw + blockDim.x - 1) / blockDim.x;
+    const int wa = w0 + threadIdx.x * per, wb = min(w1, wa + per - 1);
+    const uint32_t *rowB = st + plane + (size_t)(x + 1) * pitch;  // plane B, after the guard row
+    int sum = 0;
+    for (int w = wa; w <= wb; ++w) {
+        uint32_t e = 0xffffffffu;
+        if (w == w0) e &= 0xffffffffu << (a & 31);
+        if (w == w1) e = (b & 31) ? (e & (0xffffffffu >> (32 - (b & 31)))) : 0u;
+        const uint32_t cr = rowB[w];
+        sum += 2 * __popc(e & cr) - __popc(e & ~cr);
+    }
+    int acc = block_exclusive_sum(sum, sh);
+    int *out = loc + (size_t)x * Y;
+    for (int w = wa; w <= wb; ++w) {
+        const uint32_t cr = rowB[w];
+        const int cb = max(a, w * 32), ce = min(b, w * 32 + 31);
+        for (int y = cb; y <= ce; ++y) {
+            out[y] = acc;
+            acc += ((cr >> (y & 31)) & 1u) ? 2 : -1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) lz_hx_offsets_kernel(const uint32_t *st, int pitch, int Y, int r0, int r1,
+                                                            const int4 *rows, const int *loc, int *off, int ref_x,
+                                                            int ref_y) {
+    __shared__ int sh[32];
+    const int nr = r1 - r0 + 1;
+    const int per = (nr + blockDim.x - 1) / blockDim.x;
+    const int xa = r0 + threadIdx.x * per, xb = min(r1, xa + per - 1);
+    int sum = 0;
+    for (int x = xa; x <= xb; ++x) {
+        if (x > r0) {
+            const int y = rows[x].z;
+            const bool cr = (st[(size_t)x * pitch + (y >> 5)] >> (y & 31)) & 1u;  // A[x-1] y
+            sum += loc[(size_t)(x - 1) * Y + y] + (cr ? -2 : 1) - loc[(size_t)x * Y + y];
+        }
+        off[x] = sum;
+    }
+    const int excl = block_exclusive_sum(sum, sh);
+    for (int x = xa; x <= xb; ++x) off[x] += excl;
+    __syncthreads();
+    const int shift = off[ref_x] + loc[(size_t)ref_x * Y + ref_y];
+    __syncthreads();
+    for (int x = xa; x <= xb; ++x) off[x] -= shift;
+}
+
+template <bool SUM>
+__global__ void __launch_bounds__(256) lz_hx_finish_kernel(const uint32_t *st, size_t plane, const uint32_t *dom, int X,
+                                                          int Y, int W, int pitch, int r0, int r1, const int *loc,
+                                                          const int *off, int32_t *out, long long *acc, int *flags) {
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = blockIdx.y;
+    if (y >= Y) return;
+    const int w = y >> 5;
+    const uint32_t bit = 1u << (y & 31);
+    const bool in = x >= r0 && x <= r1 && (lz_in_mask(dom, X, W, pitch, x, w) & bit);
+    int v = 0;
+    if (in) {
+        const size_t dp = (size_t)X * pitch;
+        const uint32_t *exA = dom + 3 * dp, *exC = dom + 5 * dp;
+        v = off[x] + loc[(size_t)x * Y + y];
+        if (x > 0 && (lz_word(exA, pitch, x - 1, w) & bit)) {  // a[x-1, y]: (x-1, y) -> (x, y)
+            const bool cr = st[(size_t)x * pitch + w] & bit;
+            if (v - (off[x - 1] + loc[(size_t)(x - 1) * Y + y]) != (cr ? -2 : 1)) atomicExch(flags, 1);
+        }
+        if (lz_word(exC, pitch, x, w) & bit) {  // c[x, y]: (x+1, y-1) -> (x, y)
+            const bool cr = st[2 * plane + (size_t)(x + 1) * pitch + w] & bit;
+            if (v - (off[x + 1] + loc[(size_t)(x + 1) * Y + y - 1]) != (cr ? -2 : 1)) atomicExch(flags, 1);
+        }
+    }
+    if (SUM) acc[(size_t)x * Y + y] += v;
+    else out[(size_t)x * Y + y] = v;
+}
+
+__global__ void lz_add_heights(const int32_t *h, size_t n, long long *acc) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) acc[i] += h[i];
+}
+
+int lz_hx_scratch(tsb_loz *h) {
+    if (h->hx_h) return TSB_OK;
+    const size_t nv = (size_t)h->X * h->Y;
+    TSB_CUDA(cudaMalloc(&h->hx_h, nv * sizeof(int)));
+    TSB_CUDA(cudaMalloc(&h->hx_flags, 4 * sizeof(int)));
+    TSB_CUDA(cudaMalloc(&h->hx_off, h->X * sizeof(int)));
+    TSB_CUDA(cudaMalloc(&h->hx_rows, h->X * sizeof(int4)));
+    return TSB_OK;
+}
+
+
+int lz_hx_classify(tsb_loz *h) {
+    if (h->hx_scan >= 0) return TSB_OK;
+    int rc = lz_hx_scratch(h);
+    if (rc) return rc;
+    lz_hx_rows_kernel<<<h->X, 256, 0, h->stream>>>(h->dom, h->X, h->W, h->pitch, h->hx_rows);
+    TSB_CUDA(cudaGetLastError());
+    std::vector<int4> rows(h->X);
+    TSB_CUDA(cudaMemcpyAsync(rows.data(), h->hx_rows, sizeof(int4) * h->X, cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    int r0 = -1, r1 = -1;
+    bool ok = true;
+    for (int x = 0; x < h->X; ++x) {
+        if (rows[x].x > rows[x].y) continue;
+        if (r0 < 0) r0 = x;
+        else if (r1 != x - 1 || rows[x].z < 0) ok = false;
+        if (!rows[x].w) ok = false;
+        r1 = x;
+    }
+    h->hx_r0 = r0 < 0 ? 0 : r0;
+    h->hx_r1 = r0 < 0 ? -1 : r1;
+    h->hx_scan = (ok && r0 >= 0) ? 1 : 0;
+    const char *env = getenv("TSB_HEIGHTS_RELAX");  // test knob: force the relaxation path
+    if (env && env[0] == '1') h->hx_scan = 0;
+    return TSB_OK;
+}
+
+
+// heights of one chain into dout (device) or added to acc
+int lz_heights_dev(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *dout, long long *acc) {
+    int rc = lz_hx_classify(h);
+    if (rc) return rc;
+    const size_t nv = (size_t)h->X * h->Y;
+    const uint32_t *st = h->buf[h->cur] + (size_t)chain * h->chain_words;
+    int hf = 0;
+    if (h->hx_scan == 1 && ref_x >= h->hx_r0 && ref_x <= h->hx_r1) {
+        TSB_CUDA(cudaMemsetAsync(h->hx_flags, 0, sizeof(int), h->stream));
+        lz_hx_local_kernel<<<h->hx_r1 - h->hx_r0 + 1, 256, 0, h->stream>>>(st, h->plane, h->pitch, h->Y, h->hx_r0,
+                                                                           h->hx_rows, h->hx_h);
+        lz_hx_offsets_kernel<<<1, 1024, 0, h->stream>>>(st, h->pitch, h->Y, h->hx_r0, h->hx_r1, h->hx_rows, h->hx_h,
+                                                        h->hx_off, ref_x, ref_y);
+        const dim3 g((h->Y + 255) / 256, h->X);
+        if (acc)
+            lz_hx_finish_kernel<true><<<g, 256, 0, h->stream>>>(st, h->plane, h->dom, h->X, h->Y, h->W, h->pitch,
+                                                                h->hx_r0, h->hx_r1, h->hx_h, h->hx_off, nullptr, acc,
+                                                                h->hx_flags);
+        else
+            lz_hx_finish_kernel<false><<<g, 256, 0, h->stream>>>(st, h->plane, h->dom, h->X, h->Y, h->W, h->pitch,
+                                                                 h->hx_r0, h->hx_r1, h->hx_h, h->hx_off, dout, nullptr,
+                                                                 h->hx_flags);
+        TSB_CUDA(cudaGetLastError());
+        TSB_CUDA(cudaMemcpyAsync(&hf, h->hx_flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        TSB_CUDA(cudaStreamSynchronize(h->stream));
+        if (hf) return fail(TSB_E_INCONSISTENT, "height propagation inconsistent");
+        return TSB_OK;
+    }
+    bool overflow = false;
+    if ((rc = lz_relax<0>(h, h->hx_h, (size_t)ref_x * h->Y + ref_y, st, h->hx_flags, &overflow))) return rc;
+    if (overflow) return fail(TSB_E_INCONSISTENT, "height propagation inconsistent");
+    int32_t *o = dout;
+    if (acc) {
+        if ((rc = lz_bytes(h, nv * sizeof(int32_t)))) return rc;
+        o = reinterpret_cast<int32_t *>(h->bytes);
+    }
+    TSB_CUDA(cudaMemsetAsync(h->hx_flags, 0, sizeof(int), h->stream));
+    lz_finish<<<dim3((h->Y + 127) / 128, h->X), 128, 0, h->stream>>>(h->hx_h, h->dom, h->X, h->Y, h->pitch, o, kLzInf,
+                                                                   h->hx_flags);
+    if (acc) lz_add_heights<<<(unsigned)((nv + 255) / 256), 256, 0, h->stream>>>(o, nv, acc);
+    TSB_CUDA(cudaGetLastError());
+    TSB_CUDA(cudaMemcpyAsync(&hf, h->hx_flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (hf) return fail(TSB_E_INCONSISTENT, "height propagation inconsistent");
+    return TSB_OK;
+}
+
 }  // namespace tsb
 
 using namespace tsb;
@@ -876,6 +1112,10 @@ int tsb_loz_destroy(tsb_loz *h) {
     cudaFree(h->bytes);
     cudaFree(h->flag);
     cudaFree(h->step_dev);
+    cudaFree(h->hx_h);
+    cudaFree(h->hx_flags);
+    cudaFree(h->hx_off);
+    cudaFree(h->hx_rows);
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->seed_pinned) cudaFreeHost(h->seed_pinned);
@@ -1009,32 +1249,26 @@ int tsb_loz_sync(tsb_loz *h) {
 int tsb_loz_heights(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *out) {
     if (!h || !out) return fail(TSB_E_VALUE, "null argument");
     if (chain < 0 || chain >= h->nchains) return fail(TSB_E_VALUE, "chain out of range");
+    if (ref_x < 0 || ref_y < 0 || ref_x >= h->X || ref_y >= h->Y) return fail(TSB_E_VALUE, "reference vertex outside");
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t nv = (size_t)h->X * h->Y;
-    int *dh = nullptr, *df = nullptr;
-    int32_t *dout = nullptr;
-    TSB_CUDA(cudaMalloc(&dh, nv * sizeof(int)));
-    TSB_CUDA(cudaMalloc(&dout, nv * sizeof(int32_t)));
-    TSB_CUDA(cudaMalloc(&df, 2 * sizeof(int)));
-    bool overflow = false;
-    const uint32_t *st = h->buf[h->cur] + (size_t)chain * h->chain_words;
-    int rc = lz_relax<0>(h, dh, (size_t)ref_x * h->Y + ref_y, st, df, &overflow);
-    int hf = 0;
-    if (!rc && !overflow) {
-        cudaMemsetAsync(df, 0, sizeof(int), h->stream);
-        lz_finish<<<dim3((h->Y + 127) / 128, h->X), 128, 0, h->stream>>>(dh, h->dom, h->X, h->Y, h->pitch, dout,
-                                                                       kLzInf, df);
-        cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
-        cudaMemcpyAsync(&hf, df, sizeof(int), cudaMemcpyDeviceToHost, h->stream);
-        cudaError_t e = cudaStreamSynchronize(h->stream);
-        if (e != cudaSuccess) rc = cuda_fail(e, "loz heights");
-    }
-    cudaFree(dh);
-    cudaFree(dout);
-    cudaFree(df);
+    int rc = lz_bytes(h, nv * sizeof(int32_t));  // handle staging: no allocation per call
     if (rc) return rc;
-    if (overflow || hf) return fail(TSB_E_INCONSISTENT, "height propagation inconsistent");
+    int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
+    if ((rc = lz_heights_dev(h, chain, ref_x, ref_y, dout, nullptr))) return rc;
+    TSB_CUDA(cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
     return TSB_OK;
+}
+
+int tsb_loz_height_sum_add(tsb_loz *h, int chain0, int n, int ref_x, int ref_y, long long *acc_dev) {
+    int rc = lz_check(h, chain0, n);
+    if (rc || n == 0) return rc;
+    if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");
+    if (ref_x < 0 || ref_y < 0 || ref_x >= h->X || ref_y >= h->Y) return fail(TSB_E_VALUE, "reference vertex outside");
+    TSB_CUDA(cudaSetDevice(h->device));
+    for (int k = 0; k < n && !rc; ++k) rc = lz_heights_dev(h, chain0 + k, ref_x, ref_y, nullptr, acc_dev);
+    return rc;
 }
 
 int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int ref_y) {
@@ -1043,12 +1277,11 @@ int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int re
         return fail(TSB_E_VALUE, "chain out of range");
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t nv = (size_t)h->X * h->Y;
-    int *dh = nullptr, *df = nullptr;
-    int32_t *dout = nullptr;
-    TSB_CUDA(cudaMalloc(&dh, nv * sizeof(int)));
-    TSB_CUDA(cudaMalloc(&dout, nv * sizeof(int32_t)));
-    TSB_CUDA(cudaMalloc(&df, 2 * sizeof(int)));
-    int rc = TSB_OK;
+    int rc = lz_hx_scratch(h);
+    if (!rc) rc = lz_bytes(h, nv * sizeof(int32_t));
+    if (rc) return rc;
+    int *dh = h->hx_h, *df = h->hx_flags;
+    int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
     bool untileable = false;
     for (int pass = 0; pass < 2 && !rc && !untileable; ++pass) {
         bool overflow = false;
@@ -1070,9 +1303,6 @@ int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int re
         if (e != cudaSuccess) { rc = cuda_fail(e, "loz extremal"); break; }
         if (hf[0] || hf[1]) untileable = true;
     }
-    cudaFree(dh);
-    cudaFree(dout);
-    cudaFree(df);
     if (rc) return rc;
     if (untileable) return fail(TSB_E_UNTILEABLE, "triangle domain is not tileable");
     return TSB_OK;

@@ -103,6 +103,47 @@ __global__ void cc_count_roots(const int *L, int64_t n, unsigned long long *coun
     if ((threadIdx.x & 31) == 0 && k) atomicAdd(count, k);
 }
 
+// TriDomain checks (lozenge.py:185-210): triangle ids up(x,y) = x*sy + y,
+// down(x,y) = n + x*sy + y; up(x,y) is edge-adjacent to down(x,y),
+// down(x-1,y) and down(x,y-1) (lozenge.py:172-178 _neighbors).
+__global__ void tri_init(const uint8_t *up, const uint8_t *down, int64_t n, int *L) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        L[i] = up[i] ? (int)i : -1;
+        L[n + i] = down[i] ? (int)(n + i) : -1;
+    }
+}
+
+__global__ void tri_merge(int sx, int sy, int *L) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)sx * sy;
+    if (i >= n || L[i] < 0) return;
+    const int x = (int)(i / sy), y = (int)(i % sy);
+    if (L[n + i] >= 0) uf_unite(L, (int)i, (int)(n + i));
+    if (x > 0 && L[n + i - sy] >= 0) uf_unite(L, (int)i, (int)(n + i - sy));
+    if (y > 0 && L[n + i - 1] >= 0) uf_unite(L, (int)i, (int)(n + i - 1));
+}
+
+// Euler characteristic V - E + F over the (sx+1) x (sy+1) vertex grid, the
+// same edge sets as lozenge.py:197-210: a(x,y) = up(x,y) | down(x,y-1),
+// b(x,y) = up(x,y) | down(x-1,y), c(x,y) = up(x,y-1) | down(x,y-1).
+__global__ void tri_euler(const uint8_t *up, const uint8_t *down, int sx, int sy, long long *chi) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int Y = sy + 1;
+    int v = 0;
+    if (i < (int64_t)(sx + 1) * Y) {
+        const int x = (int)(i / Y), y = (int)(i % Y);
+        auto U = [&](int a, int b) { return a >= 0 && b >= 0 && a < sx && b < sy && up[(size_t)a * sy + b]; };
+        auto D = [&](int a, int b) { return a >= 0 && b >= 0 && a < sx && b < sy && down[(size_t)a * sy + b]; };
+        const bool vert = U(x, y) || U(x - 1, y) || U(x, y - 1) || D(x - 1, y) || D(x, y - 1) || D(x - 1, y - 1);
+        const int e = (U(x, y) || D(x, y - 1)) + (U(x, y) || D(x - 1, y)) + (U(x, y - 1) || D(x, y - 1));
+        const int f = U(x, y) + D(x, y);
+        v = (int)vert - e + f;
+    }
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long *>(chi), (unsigned long long)(long long)v);
+}
+
 }  // namespace tsb
 
 using namespace tsb;
@@ -141,6 +182,48 @@ int tsb_grid_components(int device, const uint8_t *grid, int rows, int cols, int
     cudaFree(dc);
     if (e != cudaSuccess) return cuda_fail(e, "grid components");
     *ncomp = (int64_t)k;
+    return TSB_OK;
+}
+
+int tsb_tri_check(int device, const uint8_t *up, const uint8_t *down, int sx, int sy, int64_t *ncomp,
+                  int64_t *euler) {
+    if (!up || !down || !ncomp || !euler || sx < 1 || sy < 1) return fail(TSB_E_VALUE, "bad triangle grids");
+    const int64_t n = (int64_t)sx * sy;
+    if (2 * n >= (1ll << 31)) return fail(TSB_E_CAPACITY, "%lld triangles exceed 2^31", (long long)(2 * n));
+    int rc = ensure_device(device);
+    if (rc) return rc;
+    uint8_t *du = nullptr;
+    int *L = nullptr;
+    unsigned long long *dc = nullptr;
+    long long *dchi = nullptr;
+    cudaError_t e = cudaMalloc(&du, 2 * n);
+    if (e == cudaSuccess) e = cudaMalloc(&L, sizeof(int) * 2 * n);
+    if (e == cudaSuccess) e = cudaMalloc(&dc, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&dchi, sizeof(long long));
+    if (e == cudaSuccess) e = cudaMemcpy(du, up, n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(du + n, down, n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dc, 0, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(dchi, 0, sizeof(long long));
+    if (e == cudaSuccess) {
+        const unsigned b1 = (unsigned)((n + 255) / 256), b2 = (unsigned)((2 * n + 255) / 256);
+        const int64_t nv = (int64_t)(sx + 1) * (sy + 1);
+        tri_init<<<b1, 256>>>(du, du + n, n, L);
+        tri_merge<<<b1, 256>>>(sx, sy, L);
+        cc_count_roots<<<b2, 256>>>(L, 2 * n, dc);
+        tri_euler<<<(unsigned)((nv + 255) / 256), 256>>>(du, du + n, sx, sy, dchi);
+        e = cudaGetLastError();
+    }
+    unsigned long long k = 0;
+    long long chi = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&k, dc, sizeof k, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&chi, dchi, sizeof chi, cudaMemcpyDeviceToHost);
+    cudaFree(du);
+    cudaFree(L);
+    cudaFree(dc);
+    cudaFree(dchi);
+    if (e != cudaSuccess) return cuda_fail(e, "triangle domain check");
+    *ncomp = (int64_t)k;
+    *euler = (int64_t)chi;
     return TSB_OK;
 }
 

@@ -53,6 +53,35 @@ inline uint64_t threshold_of(double p) {
     return (uint64_t)c;
 }
 
+// Block-wide reduction (all threads get the result); sh holds one slot per warp.
+template <typename T, typename Op>
+__device__ T block_reduce(T v, Op op, T *sh) {
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    v = sh[0];
+    for (int i = 1; i < nw; ++i) v = op(v, sh[i]);
+    return v;
+}
+
+// Block-wide exclusive prefix sum of one int per thread (sh: one slot per warp).
+__device__ __forceinline__ int block_exclusive_sum(int v, int *sh) {
+    int incl = v;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    __syncthreads();
+    if (lane == 31) sh[wid] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int i = 0; i < wid; ++i) base += sh[i];
+    return base + incl - v;
+}
+
 void set_error(const char *fmt, ...);
 int fail(int code, const char *fmt, ...);
 int cuda_fail(cudaError_t e, const char *what);

@@ -24,6 +24,8 @@ from .errors import CoverageError, DomainError, InconsistencyError, OutOfDomainE
 from .lattice import Uniform, VolumeWeights
 from .sweeps import Backend
 
+_TRI_DEVICE_CELLS = 1 << 16  # TriDomain checks on the GPU above this many cells (when present)
+
 Triangle = tuple[str, int, int]
 Lozenge = tuple[Triangle, Triangle]
 
@@ -110,8 +112,27 @@ class TriDomain:
         object.__setattr__(self, "down", down)
         if not (up.any() or down.any()):
             raise DomainError("domain has no triangles")
-        self._check_connected()
-        self._check_simply_connected()
+        if up.size > _TRI_DEVICE_CELLS and _native.has_device():
+            self._check_device()
+        else:
+            self._check_connected()
+            self._check_simply_connected()
+
+    def _check_device(self):
+        """Both checks of lozenge.py:185-210 on the GPU (tsb_tri_check:
+        union-find over the triangle graph, Euler characteristic V - E + F)."""
+        import ctypes
+
+        sx, sy = self.size
+        u = np.ascontiguousarray(self.up, dtype=np.uint8)
+        d = np.ascontiguousarray(self.down, dtype=np.uint8)
+        k, chi = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(_native.lib().tsb_tri_check(_native.device(), _native.ptr(u), _native.ptr(d), sx, sy,
+                                                  ctypes.byref(k), ctypes.byref(chi)))
+        if k.value != 1:
+            raise DomainError("triangles are not edge-connected")
+        if chi.value != 1:
+            raise DomainError("triangle set is not simply connected")
 
     def triangle_in(self, tri: Triangle) -> bool:
         kind, x, y = tri

@@ -42,15 +42,18 @@ class DensityMap:
 class DeviceDensity:
     """Accumulates an indicator observable of a handle's chains on the device.
 
-    `handle` is a DominoHandle ("domino-orientation") or a SixVertexHandle
-    ("h-edge", "v-edge", "c-vertex", or "height" for the mean height
-    function).  Each `add(chain0, n)` adds the current states of chains
-    [chain0, chain0 + n).
+    `handle` is a DominoHandle ("domino-orientation", or "height" for the
+    mean height function of lattice.py:537-551), a SixVertexHandle ("h-edge",
+    "v-edge", "c-vertex", "height") or a LozengeHandle ("height", the mean of
+    loz_heights, lozenge.py:414-447).  Each `add(chain0, n)` adds the current
+    states of chains [chain0, chain0 + n); heights are summed exactly in int64
+    and divided once in `result()`.
     """
 
     def __init__(self, handle, observable: str):
         import torch
 
+        from .lozenge import LozengeHandle
         from .sixvertex import SixVertexHandle
         from .sweeps import DominoHandle
 
@@ -59,11 +62,22 @@ class DeviceDensity:
         self.samples = 0
         dev = torch.device("cuda", handle.device)
         if isinstance(handle, DominoHandle):
-            if observable != "domino-orientation":
-                raise KeyError(f"unknown domino observable {observable!r}; have ['domino-orientation']")
-            nf = handle.side - 1
-            self.shape = (nf, nf)
-            self._acc = torch.zeros(self.shape, dtype=torch.int32, device=dev)
+            if observable == "height":
+                if handle.domain is None:
+                    raise ValueError("the mean height function needs the handle's domain")
+                self.shape = (handle.side, handle.side)
+                self._acc = torch.zeros(self.shape, dtype=torch.int64, device=dev)
+            elif observable == "domino-orientation":
+                nf = handle.side - 1
+                self.shape = (nf, nf)
+                self._acc = torch.zeros(self.shape, dtype=torch.int32, device=dev)
+            else:
+                raise KeyError(f"unknown domino observable {observable!r}; have ['domino-orientation', 'height']")
+        elif isinstance(handle, LozengeHandle):
+            if observable != "height":
+                raise KeyError(f"unknown lozenge observable {observable!r}; have ['height']")
+            self.shape = (handle.X, handle.Y)
+            self._acc = torch.zeros(self.shape, dtype=torch.int64, device=dev)
         elif isinstance(handle, SixVertexHandle):
             n = handle.n
             shapes = {"h-edge": (n, n + 1), "v-edge": (n + 1, n), "c-vertex": (n, n), "height": (n + 1, n + 1)}
@@ -77,14 +91,21 @@ class DeviceDensity:
         torch.cuda.synchronize(dev)  # the zeroed buffer is visible to the handle's stream
 
     def add(self, chain0: int = 0, n: int | None = None) -> None:
+        from .lozenge import LozengeHandle
         from .sweeps import DominoHandle
 
         h = self.handle
         n = h.nchains - chain0 if n is None else n
         L = _native.lib()
         p = self._acc.data_ptr()
-        if isinstance(h, DominoHandle):
+        if isinstance(h, DominoHandle) and self.observable == "height":
+            r, c = h.domain.reference_vertex
+            _native.check(L.tsb_domino_height_sum_add(h._h, chain0, n, int(r), int(c), p))
+        elif isinstance(h, DominoHandle):
             _native.check(L.tsb_domino_orientation_add(h._h, chain0, n, p))
+        elif isinstance(h, LozengeHandle):
+            x, y = h.domain.reference_vertex
+            _native.check(L.tsb_loz_height_sum_add(h._h, chain0, n, int(x), int(y), p))
         elif self.observable == "height":
             _native.check(L.tsb_sv_height_sum_add(h._h, chain0, n, p))
         else:
