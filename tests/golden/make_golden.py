@@ -306,8 +306,79 @@ def make_cli():
         print(f"cli {name}: {os.path.getsize(out)} B")
 
 
+# ------------------------------------------ six-vertex non-DWBC boundaries
+def _boundary_from_heights(h):
+    dh = h[:-1, :] - h[1:, :]
+    dv = h[:, 1:] - h[:, :-1]
+    he, ve = dh == 1, dv == 1
+    n = h.shape[0] - 1
+    return ts.Boundary(n, top=ve[0, :], bottom=ve[n, :], left=he[:, 0], right=he[:, n])
+
+
+def make_sv_boundaries():
+    """General boundaries (sixvertex.py:83-120) through sv_extremal
+    (534-562), including InfeasibleBoundary from _ring_heights (527) and
+    from the compatibility check (557), a walk from each feasible h_max and
+    h_min, and sv_cftp on small general boundaries."""
+    from tilesampler.errors import InfeasibleBoundary
+
+    rng_ = np.random.default_rng(20261017)
+    arrays, meta = {}, []
+    cases = []
+    for n in (1, 2, 3, 5, 8, 13, 40, 97):
+        for _ in range(3):
+            # min of two separable +-1 walks: a valid height function
+            hs = []
+            for _ in range(2):
+                f = np.concatenate([[0], np.cumsum(rng_.choice([-1, 1], n))])
+                g = np.concatenate([[0], np.cumsum(rng_.choice([-1, 1], n))])
+                hs.append(f[:, None] + g[None, :])
+            cases.append(_boundary_from_heights(np.minimum(hs[0], hs[1] + 2 * rng_.integers(-2, 3))))
+    # random occupancies (mostly infeasible: ring does not close or is incompatible)
+    for n in (2, 3, 4, 6, 10, 31):
+        for _ in range(4):
+            b = [rng_.random(n) < 0.5 for _ in range(4)]
+            cases.append(ts.Boundary(n, *b))
+    # rings that close but are mutually incompatible (sixvertex.py:557): the
+    # top ring peaks mid-row while the bottom ring dips, further apart in
+    # height than in distance
+    for n in (4, 6, 10, 17):
+        half = np.arange(n) < n // 2
+        ones = np.ones(n, bool)
+        cases.append(ts.Boundary(n, top=half, bottom=~half, left=ones, right=ones))
+        cases.append(ts.Boundary(n, top=~half, bottom=half, left=~ones, right=~ones))
+    w = ts.SVWeights(1.0, 1.0, 1.5)
+    for i, b in enumerate(cases):
+        for k in ("top", "bottom", "left", "right"):
+            arrays[f"b{i}_{k}"] = getattr(b, k)
+        try:
+            hi, lo = ts.sv_extremal(b.n, b)
+        except InfeasibleBoundary as e:
+            meta.append(dict(n=b.n, error=type(e).__name__, message=str(e)))
+            continue
+        arrays[f"b{i}_hi"] = hi.heights
+        arrays[f"b{i}_lo"] = lo.heights
+        start = np.stack([hi.heights, lo.heights])
+        out = sv_random_walk_batch(start, np.array([7 + i, 7 + i], dtype=np.uint64), 60, w)
+        arrays[f"b{i}_walk"] = out
+        meta.append(dict(n=b.n, error=None))
+    # CFTP on small general boundaries
+    cftp = []
+    for j, i in enumerate([k for k, m in enumerate(meta) if m["error"] is None and 3 <= m["n"] <= 8][:4]):
+        b = cases[i]
+        trace = ts.CftpTrace()
+        res = ts.sv_cftp(b.n, b, w, 0x5EED + j, count=3, trace=trace)
+        arrays[f"c{j}_h"] = np.stack([ts.heights_from_config(c).heights for c in res])
+        cftp.append(dict(case=i, master=0x5EED + j, collapsed_at=trace.collapsed_at))
+    save("sv_boundaries.npz", **arrays)
+    with open(os.path.join(HERE, "sv_boundaries.json"), "w") as f:
+        json.dump(dict(cases=meta, cftp=cftp, weights=[1.0, 1.0, 1.5], walk_steps=60), f, indent=1)
+    print("sv boundaries:", sum(m["error"] is None for m in meta), "feasible of", len(meta),
+          sorted(set(m.get("message", "") for m in meta)))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "domino", "extremal", "cftp", "sixvertex", "lozenge", "observables", "archives",
-                             "cli"]
+                             "cli", "sv_boundaries"]
     for w in which:
         globals()[f"make_{w}"]()

@@ -120,3 +120,25 @@ def test_oracle_observables_match_reference():
     assert np.array_equal(np.mean(ve, axis=0), g["sv_v_edge"])
     assert np.array_equal(np.mean(cv, axis=0), g["sv_c_vertex"])
     assert [int(c.sum()) for c in cv] == list(g["sv_ccount"])
+
+
+def test_sixvertex_general_boundaries():
+    """The oracle's six-vertex walk on the reference's non-DWBC golden walks
+    (make_golden.py make_sv_boundaries): the sweep does not depend on DWBC."""
+    import json
+
+    import paper_1804_07250_b200 as ts
+
+    g = load("sv_boundaries.npz")
+    with open(os.path.join(G, "sv_boundaries.json")) as f:
+        meta = json.load(f)
+    table = ts.SVWeights(*meta["weights"]).table()
+    k = 0
+    for i, m in enumerate(meta["cases"]):
+        if m["error"]:
+            continue
+        start = np.stack([g[f"b{i}_hi"], g[f"b{i}_lo"]])
+        out = oracle.sv_walk(start, [7 + i, 7 + i], table, meta["walk_steps"])
+        assert np.array_equal(out, g[f"b{i}_walk"]), i
+        k += 1
+    assert k >= 20

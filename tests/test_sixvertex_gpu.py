@@ -166,3 +166,42 @@ def test_tiny_and_word_edge_sizes_vs_oracle(n):
     assert np.array_equal(out, oracle.sv_walk(start, seeds, w.table(), 150))
     if n == 1:
         assert np.array_equal(out, start)
+
+
+def test_general_boundaries_golden():
+    """Non-DWBC boundaries (sixvertex.py:83-120) through the device
+    sv_extremal (534-562): extremal heights, both InfeasibleBoundary paths
+    (ring not closing, 527; mutually incompatible ring, 557) with the
+    reference's messages, walks from h_max / h_min and sv_cftp -- all against
+    reference-generated goldens (make_golden.py make_sv_boundaries)."""
+    import json
+
+    from paper_1804_07250_b200.sixvertex import sv_random_walk_batch
+
+    g = load("sv_boundaries.npz")
+    with open(os.path.join(G, "sv_boundaries.json")) as f:
+        meta = json.load(f)
+    w = ts.SVWeights(*meta["weights"])
+    bounds = []
+    for i, m in enumerate(meta["cases"]):
+        b = ts.Boundary(m["n"], *(g[f"b{i}_{k}"] for k in ("top", "bottom", "left", "right")))
+        bounds.append(b)
+        if m["error"]:
+            with pytest.raises(ts.InfeasibleBoundary, match=m["message"]):
+                ts.sv_extremal(b.n, b)
+            continue
+        hi, lo = ts.sv_extremal(b.n, b)
+        assert np.array_equal(hi.heights, g[f"b{i}_hi"]), i
+        assert np.array_equal(lo.heights, g[f"b{i}_lo"]), i
+        start = np.stack([hi.heights, lo.heights])
+        out = sv_random_walk_batch(start, np.array([7 + i, 7 + i], dtype=np.uint64), meta["walk_steps"], w)
+        assert np.array_equal(out, g[f"b{i}_walk"]), i
+    assert sum(m["error"] is None for m in meta["cases"]) >= 20
+    assert {m.get("message") for m in meta["cases"]} >= {"boundary ring heights do not close up",
+                                                         "ring heights are mutually incompatible"}
+    for j, c in enumerate(meta["cftp"]):
+        b = bounds[c["case"]]
+        trace = ts.CftpTrace()
+        res = ts.sv_cftp(b.n, b, w, c["master"], count=3, trace=trace)
+        assert np.array_equal(np.stack([ts.heights_from_config(x).heights for x in res]), g[f"c{j}_h"]), j
+        assert trace.collapsed_at == c["collapsed_at"]
