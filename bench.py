@@ -244,6 +244,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def strips_mode(args, world: int) -> bool:
+    """N > 1: one strip-sharded chain (strong scaling) or replicas (weak)."""
+    mode = "replicas" if args.replicas else args.mode
+    if mode == "auto":
+        mode = "strips" if args.order > 8192 else "replicas"
+    return world > 1 and mode == "strips"
+
+
+def bench_config(args, world: int, strips: bool) -> dict:
+    """The `config` object both arms print (identical for the same flags)."""
+    black, white = aztec_counts(args.order)
+    return {"workload": f"aztec{args.order}_uniform_from_Tmax", "order": args.order,
+            "domain_vertices": black + white, "sweeps_per_step": args.sweeps_per_step, "seed": SEED,
+            "parallelism": (f"strips x{world}, halo {args.halo} rows exchanged every {args.halo} sweeps "
+                            + ("(host NCCL p2p)" if args.host_exchange else "(device push/pull over peer memory)")
+                            if strips else (f"replicas x{world}" if world > 1 else "single chain")),
+            "l2": "flushed (256 MiB write) between timed steps; state planes stay "
+                  "L2-resident within a step by design"}
+
+
 def cpu_baseline(order: int, budget_s: float = 12.0):
     """The reference algorithm's CPU path (oracle/ C port of _kernels.py
     domino_walk, pthread row bands over all host threads) on a bounded sample."""
@@ -274,11 +294,8 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     p_up = np.full(t_max.shape, 0.5)
     s = t_max[None].copy()
-    t0 = time.perf_counter()
-    s = oracle.domino_walk(s, [SEED], p_up, 1, threads=threads)
-    one = time.perf_counter() - t0
-    per_step = max(1, int(3.0 / max(one, 1e-6)))  # ~3 s of CPU work per step
-    step = 1
+    per_step = args.sweeps_per_step  # the same step as the GPU arm (1000 sweeps: ~5 s on 16 host threads)
+    step = 0
     for _ in range(args.warmup):
         s = oracle.domino_walk(s, [SEED], p_up, per_step, step0=step, threads=threads)
         step += per_step
@@ -297,8 +314,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": {"workload": f"aztec{args.order}_uniform_from_Tmax",
-                                        "sweeps_per_step": per_step},
+        "data": "synthetic: Aztec diamond from the closed-form T_max, uniform weights",
+        "config": bench_config(args, args.gpus, strips_mode(args, args.gpus)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                          "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -359,10 +376,7 @@ def main():
     S = args.sweeps_per_step
     stream = torch.cuda.current_stream()
 
-    mode = "replicas" if args.replicas else args.mode
-    if mode == "auto":
-        mode = "strips" if args.order > 8192 else "replicas"
-    strips = world > 1 and mode == "strips"
+    strips = strips_mode(args, world)
     if strips:
         seed = SEED  # one chain sharded over all GPUs
     h = DominoHandle(d, d.n + 1, 1)
@@ -544,13 +558,7 @@ def main():
                if shared_gpu else {}),
             "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic: Aztec diamond from the closed-form T_max, uniform weights",
-            "config": {"workload": f"aztec{args.order}_uniform_from_Tmax", "order": args.order,
-                       "domain_vertices": n_domain, "sweeps_per_step": S, "seed": SEED,
-                       "parallelism": (f"strips x{world}, halo {args.halo} rows exchanged every {args.halo} sweeps "
-                                       + ("(host NCCL p2p)" if args.host_exchange else "(device push/pull over peer memory)")
-                                       if strips else (f"replicas x{world}" if world > 1 else "single chain")),
-                       "l2": "flushed (256 MiB write) between timed steps; state planes stay "
-                             "L2-resident within a step by design"},
+            "config": bench_config(args, world, strips),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic("domino_multi_kernel"),
                          "traffic_source": "profiles/traffic.json (ncu --set full capture)",
