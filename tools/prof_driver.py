@@ -26,6 +26,7 @@ def main():
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--warm", type=int, default=2000)
     p.add_argument("--sweeps", type=int, default=64)
+    p.add_argument("--state", default="", help="dom: start from this warm-state npz (tools/make_warm_state.py)")
     a = p.parse_args()
     import torch
 
@@ -57,7 +58,13 @@ def main():
         t_max, _ = aztec_extremal_states(n)
         h = DominoHandle(d, d.n + 1, 1)
         h.set_plan(ts.SweepPlan(d))
-        h.upload(t_max[None])
+        if a.state:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from make_warm_state import load
+
+            h.upload(load(a.state)[None])
+        else:
+            h.upload(t_max[None])
     h.walk([0x5EED], a.warm)
     h.walk([0x5EED], a.sweeps, step0=a.warm)
     torch.cuda.synchronize()
