@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--sweeps-per-step", type=int, default=1000)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-warm", action="store_true", help="skip the equilibrating-state sub-record")
     p.add_argument("--mode", default="auto", choices=["auto", "replicas", "strips"],
                    help="N>1: independent chains per GPU (weak scaling) or one strip-sharded chain "
                         "(strong scaling); auto = strips above order 8192")
@@ -335,6 +336,58 @@ def relaunch_under_torchrun(args) -> int:
     return subprocess.call(cmd)
 
 
+def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed):
+    """The same step timed from the committed warm state instead of T_max
+    (bench_data/aztec4096_warm.npz: T_max + 2^24 sweeps, ~10 % of vertices
+    rotateable, i.e. the regime a sampler spends its life in; the frozen T_max
+    start has 0.3 %).  Device events per step, L2 flushed between steps."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from make_warm_state import load
+
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    path = os.path.join(ROOT, "bench_data", "aztec4096_warm.npz")
+    st = load(path)  # raises if the fingerprint does not match
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_stream(stream.cuda_stream)
+    h.set_plan(plan)
+    h.upload(st[None])
+    S = args.sweeps_per_step
+    step = 0
+    for _ in range(args.warmup):
+        h.walk([seed], S, step0=step)
+        step += S
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    first = step
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        h.walk([seed], S, step0=step)
+        ev[k][1].record(stream)
+        step += S
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    att = attempts_for(seed, first, step - first, counts)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    a = torch.tensor([float(att)], dtype=torch.float64, device=red_dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(a, op=dist.ReduceOp.SUM)
+    fin = h.download()[0]
+    nv = counts[0] + counts[1]
+    rot = float(((fin == 3) | (fin == 12)).sum()) / nv
+    per_launch_ms = float(t.item()) / (args.steps * S / MK)
+    achieved = MK * nv / (per_launch_ms / 1e3) / 1e9
+    peak, _ = peaks()
+    return {"value": float(a.item()) / (float(t.item()) / 1e3), "unit": UNIT,
+            "ms_per_step": float(t.item()) / args.steps, "us_per_sweep": 1e3 * float(t.item()) / (args.steps * S),
+            "rotateable_frac_end": rot,
+            "roofline": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
+            "state": "bench_data/aztec4096_warm.npz (T_max + 2^24 sweeps of seed 0xA11CE, sha "
+                     + str(np.load(path)["sha"]) + ")"}
+
+
 def main():
     args = parse()
     world_env = os.environ.get("WORLD_SIZE")
@@ -546,6 +599,10 @@ def main():
                "serial_one_chain": serial * world,
                "random_walk_pageable": att_plain / dt_plain}
 
+    warm = None
+    if not args.no_warm and not strips and args.order == 4096:
+        warm = warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.order)
@@ -568,6 +625,7 @@ def main():
                          "accounting": "1 B per in-domain vertex per sweep (4-bit state read + write)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "warm": warm,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (S // walk_len) * (launches_per_walk(walk_len)
                                                            + (3 if strips and not args.host_exchange else 0)),  # + push/pull/epoch

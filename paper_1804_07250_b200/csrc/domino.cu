@@ -175,6 +175,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TT(ph)
 #endif
 
+// Coins whose outcome cannot reach a stored bit are not drawn.  Row k's fire
+// row touches rows k-1 and k, and the fire test of a row reads the row above,
+// so sweep s of a kMK = 2 tile needs fire rows s+1 .. kMRows-1-s; across
+// columns a fire moves one column per sweep, so the left halo word (lane 0,
+// word a) matters only at bit 31 in sweep 0, the right halo word (lane 31,
+// word b) at bits 0-1 in sweep 0 and bit 0 in sweep 1.  Skipped sites keep
+// their state; they lie in the stale halo, which is never stored.
+static_assert(kMK == 2, "need masks are derived for two sweeps per launch");
+__device__ __forceinline__ uint32_t need_a(int s, int k, int lane) {
+    if (k < s + 1 || k > kMRows - 1 - s) return 0u;
+    return lane == 0 ? (s == 0 ? 0x80000000u : 0u) : 0xFFFFFFFFu;
+}
+__device__ __forceinline__ uint32_t need_b(int s, int k, int lane) {
+    if (k < s + 1 || k > kMRows - 1 - s) return 0u;
+    return lane == 31 ? (s == 0 ? 3u : 1u) : 0xFFFFFFFFu;
+}
+
 // kMK sweeps of one tile held in registers (cur) and shared memory, then the
 // exact central rows are stored.
 template <int TM>
@@ -201,10 +218,10 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vua & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act;
+        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act & need_a(s, k, lane);
         const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
         const uint32_t ib = vub & cur.z & ~(lb | cur.w);
-        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act;
+        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act & need_b(s, k, lane);
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
@@ -351,7 +368,8 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.y, 1);  // lane 0: halo, wraps harmlessly
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vu & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act;
+        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act &
+                            (lane == 31 ? need_b(s, k, 31) : need_a(s, k, lane));
         uint32_t f = 0u;
         if (__any_sync(0xffffffffu, ra != 0u)) {
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
@@ -1230,7 +1248,7 @@ int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states) {
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t grid = (size_t)h->side * h->side;
     if ((rc = ensure_bytes(h, grid * n))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(h->bytes, states, grid * n, cudaMemcpyHostToDevice, h->stream));
+    if ((rc = staged_h2d(h->bytes, states, grid * n, h->stream))) return rc;
     TSB_CUDA(cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
     pack_kernel<<<dim3((h->W + 127) / 128, h->side, n), 128, 0, h->stream>>>(
         h->bytes, h->side, h->W, h->pitch, h->chain_stride, h->dom,
@@ -1254,9 +1272,7 @@ int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states) {
     unpack_kernel<<<dim3((h->side + 127) / 128, h->side, n), 128, 0, h->stream>>>(
         h->buf[h->cur] + (size_t)chain0 * h->chain_stride + kPad, h->side, h->pitch, h->chain_stride, h->bytes);
     TSB_CUDA(cudaGetLastError());
-    TSB_CUDA(cudaMemcpyAsync(states, h->bytes, grid * n, cudaMemcpyDeviceToHost, h->stream));
-    TSB_CUDA(cudaStreamSynchronize(h->stream));
-    return TSB_OK;
+    return staged_d2h(states, h->bytes, grid * n, h->stream);
 }
 
 int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step0,

@@ -93,16 +93,19 @@ __global__ void __launch_bounds__(256) relax_kernel(int *h, const uint2 *st, con
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 4; ++k) orig[k] = s[ty + 8 * k + 1][tx + 1];
-    volatile int(*vs)[kTile + 2] = s;
+    // Jacobi rounds: every thread reads its neighbours, a barrier, then the
+    // improved values are written (race-free; the fixpoint is unique, so the
+    // update order does not change the result)
     bool over = false;
     for (int it = 0; it < 4 * kTile; ++it) {
         bool ch = false;
+        int nv[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int lr = ty + 8 * k;
-            const int cur = vs[lr + 1][tx + 1];
+            const int cur = s[lr + 1][tx + 1];
             int best = cur;
-            const int nb[4] = {vs[lr][tx + 1], vs[lr + 2][tx + 1], vs[lr + 1][tx], vs[lr + 1][tx + 2]};
+            const int nb[4] = {s[lr][tx + 1], s[lr + 2][tx + 1], s[lr + 1][tx], s[lr + 1][tx + 2]};
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 const int8_t w = wt[d][lr][tx];
@@ -110,15 +113,19 @@ __global__ void __launch_bounds__(256) relax_kernel(int *h, const uint2 *st, con
                 const int cand = nb[d] + w;
                 best = MODE == 2 ? max(best, cand) : min(best, cand);
             }
-            if (best != cur) {
-                if (MODE == 2 ? best > limit : best < -limit) {
-                    over = true;
-                    best = MODE == 2 ? limit : -limit;  // clamp; the run is abandoned
-                }
-                if (best != cur) {
-                    vs[lr + 1][tx + 1] = best;
-                    ch = true;
-                }
+            if (best != cur && (MODE == 2 ? best > limit : best < -limit)) {
+                over = true;
+                best = MODE == 2 ? limit : -limit;  // clamp; the run is abandoned
+            }
+            nv[k] = best;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int lr = ty + 8 * k;
+            if (nv[k] != s[lr + 1][tx + 1]) {
+                s[lr + 1][tx + 1] = nv[k];
+                ch = true;
             }
         }
         if (!__syncthreads_or(ch)) break;

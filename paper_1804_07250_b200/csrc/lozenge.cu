@@ -261,8 +261,17 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         const uint32_t d4a = (B.a << 1) | (bprev >> 31), d4b = (B.b << 1) | (B.a >> 31);
         const uint32_t lowa = B.a & m.x & C.a & ~A.a & ~d2a & ~d4a, lowb = B.b & m.y & C.b & ~A.b & ~d2b & ~d4b;
         const uint32_t higha = A.a & d2a & d4a & ~B.a & ~m.x & ~C.a, highb = A.b & d2b & d4b & ~B.b & ~m.y & ~C.b;
-        const uint32_t rota = (lowa | higha) & mod3_mask((b3a - cls + 3) % 3);
-        const uint32_t rotb = (lowb | highb) & mod3_mask((b3b - cls + 3) % 3);
+        // coins that cannot reach a stored bit are not drawn (as the domino
+        // tiles): fire row x touches rows x-1 and x, so sweep s needs fire rows
+        // s+1 .. kLzMRows-1-s, and a fire moves about one column per sweep, so
+        // the halo words (lane 0 word a, lane 31 word b) need only the bits
+        // within K-s (+1) columns of the interior
+        const bool need = k >= s + 1 && k <= kLzMRows - 1 - s;
+        const int reach = c.K - s;
+        const uint32_t hl = lane == 0 ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
+        const uint32_t hr = lane == 31 ? (reach >= 31 ? ~0u : (1u << (reach + 1)) - 1u) : ~0u;
+        const uint32_t rota = need ? (lowa | higha) & mod3_mask((b3a - cls + 3) % 3) & hl : 0u;
+        const uint32_t rotb = need ? (lowb | highb) & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (rota | rotb) != 0u))
             f = warp_fire<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
@@ -452,17 +461,18 @@ __global__ void __launch_bounds__(256) lz_relax_kernel(int *h, const uint32_t *s
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 4; ++q) orig[q] = s[ty + 8 * q + 1][tx + 1];
-    volatile int(*vs)[kLzT + 2] = s;
+    // Jacobi rounds (read, barrier, write): race-free, same unique fixpoint
     bool over = false;
     for (int it = 0; it < 4 * kLzT; ++it) {
         bool ch = false;
+        int nv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int lx = ty + 8 * q, ly = tx;
-            const int cur = vs[lx + 1][ly + 1];
+            const int cur = s[lx + 1][ly + 1];
             int best = cur;
-            const int nb[6] = {vs[lx][ly + 1], vs[lx + 1][ly], vs[lx + 2][ly], vs[lx + 2][ly + 1], vs[lx + 1][ly + 2],
-                               vs[lx][ly + 2]};
+            const int nb[6] = {s[lx][ly + 1], s[lx + 1][ly], s[lx + 2][ly], s[lx + 2][ly + 1], s[lx + 1][ly + 2],
+                               s[lx][ly + 2]};
 #pragma unroll
             for (int d = 0; d < 6; ++d) {
                 const int8_t w = wt[d][lx][ly];
@@ -470,15 +480,19 @@ __global__ void __launch_bounds__(256) lz_relax_kernel(int *h, const uint32_t *s
                 const int cand = nb[d] + w;
                 best = MODE == 2 ? max(best, cand) : min(best, cand);
             }
-            if (best != cur) {
-                if (MODE == 2 ? best > limit : best < -limit) {
-                    over = true;
-                    best = MODE == 2 ? limit : -limit;
-                }
-                if (best != cur) {
-                    vs[lx + 1][ly + 1] = best;
-                    ch = true;
-                }
+            if (best != cur && (MODE == 2 ? best > limit : best < -limit)) {
+                over = true;
+                best = MODE == 2 ? limit : -limit;
+            }
+            nv[q] = best;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int lx = ty + 8 * q, ly = tx;
+            if (nv[q] != s[lx + 1][ly + 1]) {
+                s[lx + 1][ly + 1] = nv[q];
+                ch = true;
             }
         }
         if (!__syncthreads_or(ch)) break;
@@ -1162,7 +1176,7 @@ int tsb_loz_upload(tsb_loz *h, int chain0, int n, const uint8_t *edges) {
     TSB_CUDA(cudaSetDevice(h->device));
     const size_t need = (size_t)n * 3 * h->X * h->Y;
     if ((rc = lz_bytes(h, need))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(h->bytes, edges, need, cudaMemcpyHostToDevice, h->stream));
+    if ((rc = staged_h2d(h->bytes, edges, need, h->stream))) return rc;
     TSB_CUDA(cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream));
     lz_pack_kernel<<<dim3((h->W + 127) / 128, h->X, n), 128, 0, h->stream>>>(
         h->bytes, h->X, h->Y, h->W, h->pitch, h->plane, h->chain_words, h->dom,
@@ -1185,9 +1199,7 @@ int tsb_loz_download(tsb_loz *h, int chain0, int n, uint8_t *edges) {
     lz_unpack_kernel<<<dim3((h->Y + 127) / 128, h->X, n), 128, 0, h->stream>>>(
         h->buf[h->cur] + (size_t)chain0 * h->chain_words, h->X, h->Y, h->pitch, h->plane, h->chain_words, h->bytes);
     TSB_CUDA(cudaGetLastError());
-    TSB_CUDA(cudaMemcpyAsync(edges, h->bytes, need, cudaMemcpyDeviceToHost, h->stream));
-    TSB_CUDA(cudaStreamSynchronize(h->stream));
-    return TSB_OK;
+    return staged_d2h(edges, h->bytes, need, h->stream);
 }
 
 static int lz_push_seeds(tsb_loz *h, int n, const uint64_t *seeds) {

@@ -254,7 +254,14 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
                  dR = __shfl_down_sync(0xffffffffu, d[0], 1);
         if (lane == 0) uL = bL = dL = 0u;
         if (lane == 31) uR = bR = dR = 0u;
-        const bool rowok = R >= 1 && R <= c.n - 1;
+        // coins that cannot reach a stored face are not drawn: a flip moves
+        // one row / column per sweep, so sweep s only needs tile rows
+        // s+1 .. TR-2-s and, in tiles with word halos, the halo bits within
+        // K-1-s columns of the interior (one column of slack each side)
+        const bool rowok = R >= 1 && R <= c.n - 1 && i >= s + 1 && i <= TR - 2 - s;
+        const int reach = c.K - s;  // K-1-s plus one column of slack
+        const uint32_t hmask_l = c.woff < 0 && lane == 0 ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
+        const uint32_t hmask_r = c.woff < 0 && lane == 31 ? (reach >= 32 ? ~0u : (1u << reach) - 1u) : ~0u;
         const int odd = (pr + pc + p0) & 1;  // parity of the class faces
         const uint32_t pcm = pc ? 0xAAAAAAAAu : 0x55555555u;
         uint32_t mn[WPL], cand[WPL], nw[WPL], ne[WPL], sw[WPL], se[WPL];
@@ -268,7 +275,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
             const uint32_t eq_u = ~(u[j] ^ b[j]), eq_d = ~(d[j] ^ b[j]), eq_l = ~(left ^ b[j]),
                            eq_r = ~(right ^ b[j]);
             const uint32_t all_eq = eq_u & eq_d & eq_l & eq_r, all_ne = ~(eq_u | eq_d | eq_l | eq_r);
-            const uint32_t act = rowok ? (cm[j] & pcm) : 0u;
+            const uint32_t act = rowok ? (cm[j] & pcm & (j == 0 ? hmask_l : ~0u) & (j == WPL - 1 ? hmask_r : ~0u)) : 0u;
             mn[j] = (odd ? all_ne : all_eq) & act;
             cand[j] = mn[j] | ((odd ? all_eq : all_ne) & act);
             nw[j] = ((u[j] << 1) | (pu >> 31)) ^ b[j];
@@ -840,8 +847,7 @@ int tsb_sv_upload(tsb_sv *h, int chain0, int n, const int32_t *heights) {
     if (rc || n == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = sv_hbuf(h, n))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(h->hbuf, heights, sizeof(int32_t) * (size_t)n * h->f * h->f, cudaMemcpyHostToDevice,
-                             h->stream));
+    if ((rc = staged_h2d(h->hbuf, heights, sizeof(int32_t) * (size_t)n * h->f * h->f, h->stream))) return rc;
     return sv_pack_dev(h, chain0, n, h->hbuf);
 }
 
@@ -851,10 +857,7 @@ int tsb_sv_download(tsb_sv *h, int chain0, int n, int32_t *heights) {
     TSB_CUDA(cudaSetDevice(h->device));
     if ((rc = sv_hbuf(h, n))) return rc;
     if ((rc = sv_unpack_dev(h, chain0, n, h->hbuf))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(heights, h->hbuf, sizeof(int32_t) * (size_t)n * h->f * h->f, cudaMemcpyDeviceToHost,
-                             h->stream));
-    TSB_CUDA(cudaStreamSynchronize(h->stream));
-    return TSB_OK;
+    return staged_d2h(heights, h->hbuf, sizeof(int32_t) * (size_t)n * h->f * h->f, h->stream);
 }
 
 static int sv_walk_impl(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uint64_t step0, uint64_t n_steps,

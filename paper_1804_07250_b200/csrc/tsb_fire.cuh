@@ -44,24 +44,43 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     }
     fres[2 * lane] = 0u;
     fres[2 * lane + 1] = 0u;
+    // pad the queue to a multiple of 32 with copies of job 0: a duplicate
+    // coin sets the same fire bit again (idempotent), and every round of the
+    // loop below then runs two independent splitmix chains per lane without
+    // a divergent tail (lanes of a warp issue together, so the padding costs
+    // no issue slots)
+    const int padded = (total + 31) & ~31;
     __syncwarp();
-    const uint64_t base = seedinfo[2 * z];
+    if (lane < padded - total) queue[total + lane] = queue[0];
+    __syncwarp();
     const uint64_t salt = (step + 1ull) * kGold;
-    // site index r * side + column; column = 32 * (wa of lane 0) + 32 * WPL * lane + 32 * word + bit
+    // site index i = r * side + column, column = 32 * (wa of lane 0) + col,
+    // col = 32 * WPL * lane' + 32 * word + bit (the job's low bits); the site
+    // key's argument base + (i + 1) * G = kb + col * G
     const uint64_t row_idx = (uint64_t)r * (uint64_t)side + (uint64_t)(int64_t)((wa - WPL * lane) * 32);
-    for (int j = lane; j < total; j += 64) {
-        const bool two = j + 32 < total;
-        const uint32_t q0 = queue[j], q1 = two ? queue[j + 32] : q0;
-        const uint64_t i0 = row_idx + (uint64_t)(q0 & 63u) + (uint64_t)(((q0 >> 6) & 31u) * (32u * WPL));
-        const uint64_t i1 = row_idx + (uint64_t)(q1 & 63u) + (uint64_t)(((q1 >> 6) & 31u) * (32u * WPL));
+    const uint64_t kb = seedinfo[2 * z] + (row_idx + 1ull) * kGold;
+    auto col_of = [](uint32_t q) -> uint32_t {
+        return WPL == 2 ? (q & 2047u) : (((q >> 6) & 31u) * (32u * WPL) + (q & 63u));
+    };
+    int j = lane;
+    for (; j + 32 < padded; j += 64) {
+        const uint32_t q0 = queue[j], q1 = queue[j + 32];
+        const uint32_t c0 = col_of(q0), c1 = col_of(q1);
         // two independent chains for ILP
-        const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
-        const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
-        const uint64_t t0 = TM == 2 ? __ldg(tgrid + i0) : t;
-        const uint64_t t1 = TM == 2 ? __ldg(tgrid + i1) : t;
+        const uint64_t x0 = mix64_hot(mix64_hot(kb + (uint64_t)c0 * kGold) + salt);
+        const uint64_t x1 = mix64_hot(mix64_hot(kb + (uint64_t)c1 * kGold) + salt);
+        const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
+        const uint64_t t1 = TM == 2 ? __ldg(tgrid + row_idx + c1) : t;
+        const bool f0 = ((x0 >> 11) < t0) == (bool)(q0 >> 11), f1 = ((x1 >> 11) < t1) == (bool)(q1 >> 11);
         // fire word of (lane', word) = fres[2 * lane' + word] (WPL = 1: word 0 only)
+        if (f0) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+        if (f1) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
+    }
+    if (j < padded) {
+        const uint32_t q0 = queue[j], c0 = col_of(q0);
+        const uint64_t x0 = mix64_hot(mix64_hot(kb + (uint64_t)c0 * kGold) + salt);
+        const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
         if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
-        if (two && ((x1 >> 11) < t1) == (bool)(q1 >> 11)) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
     }
     __syncwarp();
     return make_uint2(fres[2 * lane], fres[2 * lane + 1]);
