@@ -59,6 +59,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-warm", action="store_true", help="skip the equilibrating-state sub-record")
+    p.add_argument("--no-collapsed", action="store_true", help="skip the run-collapsing sub-record")
     p.add_argument("--mode", default="auto", choices=["auto", "replicas", "strips"],
                    help="N>1: independent chains per GPU (weak scaling) or one strip-sharded chain "
                         "(strong scaling); auto = strips above order 8192")
@@ -336,7 +337,7 @@ def relaunch_under_torchrun(args) -> int:
     return subprocess.call(cmd)
 
 
-def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed):
+def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed, collapse=False):
     """The same step timed from the committed warm state instead of T_max
     (bench_data/aztec4096_warm.npz: T_max + 2^24 sweeps, ~10 % of vertices
     rotateable, i.e. the regime a sampler spends its life in; the frozen T_max
@@ -349,6 +350,7 @@ def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dis
     path = os.path.join(ROOT, "bench_data", "aztec4096_warm.npz")
     st = load(path)  # raises if the fingerprint does not match
     h = DominoHandle(d, d.n + 1, 1)
+    h.set_collapse(collapse)
     h.set_stream(stream.cuda_stream)
     h.set_plan(plan)
     h.upload(st[None])
@@ -386,6 +388,55 @@ def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dis
             "roofline": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
             "state": "bench_data/aztec4096_warm.npz (T_max + 2^24 sweeps of seed 0xA11CE, sha "
                      + str(np.load(path)["sha"]) + ")"}
+
+
+def collapsed_record(args, d, plan, t_max, counts, stream, flush, red_dev, world, torch, dist, seed):
+    """The library default (tsb_domino_set_collapse): a sweep followed by a
+    sweep of the same colour is skipped -- the move is a heat-bath update and
+    a colour's rotateable set cannot change while only that colour moves, so
+    the last sweep of a run decides and the states are bit-identical (tests
+    run with collapsing on and off).  Reported beside, not in, the headline:
+    the attempt count is the reference's workload, about half of whose sweeps
+    are executed here.  Same steps as the headline, from T_max and from the
+    warm state."""
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_collapse(True)
+    h.set_stream(stream.cuda_stream)
+    h.set_plan(plan)
+    h.upload(t_max[None])
+    S = args.sweeps_per_step
+    step = 0
+    for _ in range(args.warmup):
+        h.walk([seed], S, step0=step)
+        step += S
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    first = step
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        h.walk([seed], S, step0=step)
+        ev[k][1].record(stream)
+        step += S
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    executed = sum(1 for s in range(first, step)
+                   if (s + 1 - first) % S == 0 or _color_at(seed, s) != _color_at(seed, s + 1))  # walk ends: never skipped
+    att = attempts_for(seed, first, step - first, counts)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    a = torch.tensor([float(att)], dtype=torch.float64, device=red_dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(a, op=dist.ReduceOp.SUM)
+    rec = {"value": float(a.item()) / (float(t.item()) / 1e3), "unit": UNIT,
+           "us_per_sweep": 1e3 * float(t.item()) / (args.steps * S),
+           "sweeps_executed_frac": executed / (step - first)}
+    if args.order == 4096 and not args.no_warm:
+        w = warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed, collapse=True)
+        rec["warm"] = {"value": w["value"], "us_per_sweep": w["us_per_sweep"]}
+    return rec
 
 
 def main():
@@ -433,6 +484,7 @@ def main():
     if strips:
         seed = SEED  # one chain sharded over all GPUs
     h = DominoHandle(d, d.n + 1, 1)
+    h.set_collapse(False)  # the headline executes every sweep (run collapsing: the "collapsed" record)
     h.set_stream(stream.cuda_stream)
     h.set_plan(plan)
     h.upload(t_max[None])
@@ -534,6 +586,7 @@ def main():
         # pinned host memory; the output of step k is the input of step k+1.
         side = d.n + 1
         he = DominoHandle(d, side, 1)
+        he.set_collapse(False)
         he.set_plan(plan)
         bufs = [torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         bufs[0].numpy()[0] = t_max
@@ -558,6 +611,7 @@ def main():
         # host checks run while chain B walks, so the copies hide behind the
         # sweeps.  Every upload, walk and download is inside the timed region.
         hs = [he, DominoHandle(d, side, 1)]
+        hs[1].set_collapse(False)
         hs[1].set_plan(plan)
         sb = [bufs[0], torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True)]
         sb[1].numpy()[0] = t_max
@@ -597,11 +651,15 @@ def main():
                       "two chains on two handles streamed so one chain's copies overlap the other's sweeps; "
                       "host wall clock",
                "serial_one_chain": serial * world,
-               "random_walk_pageable": att_plain / dt_plain}
+               "random_walk_pageable": att_plain / dt_plain,
+               "random_walk_pageable_note": "ts.random_walk on pageable numpy arrays, library defaults "
+                                            "(run collapsing on)"}
 
-    warm = None
+    warm = collapsed = None
     if not args.no_warm and not strips and args.order == 4096:
         warm = warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed)
+    if not args.no_collapsed and not strips:
+        collapsed = collapsed_record(args, d, plan, t_max, counts, stream, flush, red_dev, world, torch, dist, seed)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -626,6 +684,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "warm": warm,
+            "collapsed": collapsed,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (S // walk_len) * (launches_per_walk(walk_len)
                                                            + (3 if strips and not args.host_exchange else 0)),  # + push/pull/epoch

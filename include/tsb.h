@@ -227,6 +227,10 @@ int tsb_sv_observe_add(tsb_sv *h, int chain0, int n, int observable, uint32_t *a
 /* Face heights summed into a device int64 accumulator ((n+1)^2): the mean
  * height function = acc / (#states added). */
 int tsb_sv_height_sum_add(tsb_sv *h, int chain0, int n, long long *acc_dev);
+/* Class-run collapsing for the six-vertex walk (default on; env
+ * TSB_SV_COLLAPSE=0): the c-flip is a heat-bath move, so a sweep followed by
+ * a sweep of the same class is skipped; bit-identical results. */
+int tsb_sv_set_collapse(tsb_sv *h, int on);
 /* Archive record: h_edges then v_edges ravelled as '0'/'1' (stats.py:146-153);
  * size query as tsb_domino_serialize. */
 int tsb_sv_serialize(tsb_sv *h, int chain, char *out, size_t cap, size_t *len);
@@ -265,6 +269,9 @@ int tsb_loz_height_sum_add(tsb_loz *h, int chain0, int n, int ref_x, int ref_y, 
 /* loz_extremal (lozenge.py:762-775) into chains chain_max / chain_min;
  * TSB_E_UNTILEABLE when the domain has no tiling. */
 int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int ref_y);
+/* Class-run collapsing for the lozenge walk (default on; env
+ * TSB_LZ_COLLAPSE=0), as tsb_sv_set_collapse. */
+int tsb_loz_set_collapse(tsb_loz *h, int on);
 /* Archive record: edges (3, X, Y) ravelled as '0'/'1' (stats.py:146-153). */
 int tsb_loz_serialize(tsb_loz *h, int chain, char *out, size_t cap, size_t *len);
 int tsb_loz_coalesced(tsb_loz *h, int chain0, int npairs, uint8_t *flags);
@@ -273,6 +280,15 @@ int tsb_loz_replicate(tsb_loz *h, int src, int dst0, int step, int n);
 int tsb_loz_cftp(tsb_loz *h, const uint8_t *top0, const uint8_t *bot0, const uint64_t *masters, int count,
                  int max_doublings, uint8_t *out_edges, int32_t *collapsed_round, tsb_progress_fn progress,
                  void *user);
+
+/* Run collapsing (default on; env TSB_DOM_COLLAPSE=0 turns it off at
+ * creation): a sweep whose successor in the same walk has the same colour is
+ * skipped.  The move is a heat-bath update (_kernels.py:46-55: a rotateable
+ * vertex becomes 12 iff u < p_up, else 3, whatever its state) and a colour's
+ * rotateable set cannot change while only that colour moves, so the last
+ * sweep of a run of equal colours alone decides the state: results are
+ * bit-identical, about half of the sweeps are executed. */
+int tsb_domino_set_collapse(tsb_domino *h, int on);
 
 /* One-shot form of the fused hook: evolves a host (nchains, side, side)
  * uint8 batch in place (upload + walk + download). */

@@ -92,6 +92,7 @@ _SIGS = {
     "tsb_domino_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
     "tsb_domino_sync": (_i, [_vp]),
     "tsb_domino_set_window": (_i, [_vp, _i, _i]),
+    "tsb_domino_set_collapse": (_i, [_vp, _i]),
     "tsb_domino_row_bytes": (_i, [_vp, _vp]),
     "tsb_domino_get_rows": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_domino_set_rows": (_i, [_vp, _i, _i, _i, _vp]),
@@ -125,6 +126,7 @@ _SIGS = {
     "tsb_sv_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),
     "tsb_sv_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
     "tsb_sv_sync": (_i, [_vp]),
+    "tsb_sv_set_collapse": (_i, [_vp, _i]),
     "tsb_sv_extremal": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "tsb_sv_coalesced": (_i, [_vp, _i, _i, _vp]),
     "tsb_sv_replicate": (_i, [_vp, _i, _i, _i, _i]),
@@ -138,6 +140,7 @@ _SIGS = {
     "tsb_loz_walk": (_i, [_vp, _i, _i, _vp, _u64, _u64]),
     "tsb_loz_sweep": (_i, [_vp, _i, _i, _vp, _u64, _i]),
     "tsb_loz_sync": (_i, [_vp]),
+    "tsb_loz_set_collapse": (_i, [_vp, _i]),
     "tsb_loz_heights": (_i, [_vp, _i, _i, _i, _vp]),
     "tsb_loz_height_sum_add": (_i, [_vp, _i, _i, _i, _i, _vp]),
     "tsb_loz_extremal": (_i, [_vp, _i, _i, _i, _i]),

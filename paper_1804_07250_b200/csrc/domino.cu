@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
     uint64_t step;
     if (c.colors) {
         step = *c.step_dev + c.step;
-        color = c.colors[z * kGraphSweeps + (int)c.step];
+        color = c.colors[z * kGraphSweeps + (int)c.step] & 1;  // single sweeps are never skipped
     } else {
         step = c.step;
         color = c.color_override >= 0 ? c.color_override
@@ -202,7 +202,9 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         const uint64_t step = step0 + (uint64_t)s;
-        const int color = c.colors[z * kGraphSweeps + (int)c.step + s];
+        const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
+        if (ci & 2) continue;  // collapsed run: block-uniform
+        const int color = ci & 1;
         vs[k][lane] = make_uint2(cur.x, cur.z);
         __syncthreads();
         uint32_t vua = 0u, vub = 0u;
@@ -360,7 +362,9 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         const uint64_t step = step0 + (uint64_t)s;
-        const int color = c.colors[z * kGraphSweeps + (int)c.step + s];
+        const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
+        if (ci & 2) continue;  // collapsed run: block-uniform
+        const int color = ci & 1;
         vs[k][lane] = cur.x;
         __syncthreads();
         const uint32_t vu = k > 0 ? vs[k - 1][lane] : 0u;
@@ -408,6 +412,7 @@ struct ResCtx {
     size_t chain_stride;
     int side, pitch, W;
     uint64_t step0, n_steps;
+    int collapse;
 };
 
 // Coins of a warp's rotateable active sites, dealt round-robin to its lanes
@@ -476,6 +481,8 @@ __global__ void __launch_bounds__(kResThreads, 1) domino_resident_kernel(ResCtx 
         const uint64_t step = c.step0 + s;
         const uint64_t salt = (step + 1ull) * kGold;
         const int color = (int)(mix64(gkey + salt) >> 63);  // BLACK iff u < 1/2 (sweeps.py:266-269)
+        // collapsed run (colors_kernel): the next sweep has the same colour
+        if (c.collapse && s + 1 < c.n_steps && (int)(mix64(gkey + salt + kGold) >> 63) == color) continue;
         const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
         for (int i0 = 0; i0 < items; i0 += blockDim.x) {  // warp-uniform trip count
             const int i = i0 + threadIdx.x;
@@ -547,7 +554,9 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         const uint64_t step = step0 + (uint64_t)s;
-        const int color = c.colors[zt * kGraphSweeps + (int)c.step + s];
+        const int ci = c.colors[zt * kGraphSweeps + (int)c.step + s];
+        if (ci & 2) continue;  // collapsed run: block-uniform
+        const int color = ci & 1;
         vs[0][k][lane] = ct.x;
         vs[1][k][lane] = cb.x;
         __syncthreads();
@@ -585,11 +594,25 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx
 }
 
 // Colours of the next kGraphSweeps sweeps of every chain (graph mode).
+// Colour of every sweep of a replay (bit 0) and, with run collapsing, a
+// skip flag (bit 1): a sweep whose successor in the same walk has the same
+// colour is skipped.  The domino move is a heat-bath update -- a rotateable
+// vertex becomes 12 iff u < p_up and 3 otherwise, whatever its state
+// (_kernels.py:46-55) -- and while one colour is swept the other colour does
+// not move, so the rotateable set of that colour cannot change within a run
+// of equal colours and only the last sweep of the run decides the state.
+// Skipping the others gives the identical state (tests: every golden walk,
+// oracle walks, CFTP samples and traces, with TSB_DOM_COLLAPSE=0 and 1).
+// step_dev[0] = step of the replay's first sweep, step_dev[1] = end of the walk.
 __global__ void colors_kernel(const uint64_t *seedinfo, const uint64_t *step_dev, uint64_t offset,
-                              uint8_t *colors) {
+                              uint8_t *colors, int collapse) {
     const int z = blockIdx.x, i = threadIdx.x;
-    const uint64_t step = *step_dev + offset + (uint64_t)i;
-    colors[z * kGraphSweeps + i] = (uint8_t)(mix64(seedinfo[2 * z + 1] + (step + 1ull) * kGold) >> 63);
+    const uint64_t step = step_dev[0] + offset + (uint64_t)i;
+    const uint64_t g = seedinfo[2 * z + 1];
+    const int col = (int)(mix64(g + (step + 1ull) * kGold) >> 63);
+    int skip = 0;
+    if (collapse && step + 1ull < step_dev[1]) skip = (int)(mix64(g + (step + 2ull) * kGold) >> 63) == col;
+    colors[z * kGraphSweeps + i] = (uint8_t)(col | (skip << 1));
 }
 
 // --------------------------------------------------------------- codecs
@@ -850,6 +873,10 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
 }
 
 __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
+__global__ void set_walk_kernel(uint64_t *step_dev, uint64_t step0, uint64_t end) {
+    step_dev[0] = step0;
+    step_dev[1] = end;
+}
 __global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
 
 // canonical (band-major) order of a window's tiles [0, n): order_kernel input state
@@ -931,7 +958,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
                       h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
                       h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0 &&
-                      h->g_tail == h->graph_tail && h->g_coupled == h->coupled;
+                      h->g_tail == h->graph_tail && h->g_coupled == h->coupled && h->g_collapse == h->collapse;
     if (same) return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -941,7 +968,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     cudaGraph_t g = nullptr;
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
-    colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
+    colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
     if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost + h->win_m0, h->mtiles + h->win_m0, h->win_mn,
@@ -972,6 +999,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_winm = h->win_m0;
     h->g_tail = h->graph_tail;
     h->g_coupled = h->coupled;
+    h->g_collapse = h->collapse;
     return TSB_OK;
 }
 
@@ -1034,7 +1062,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
         return bail(e, "cudaMallocHost seeds");
     if ((e = cudaMalloc(&h->bad, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc flag");
-    if ((e = cudaMalloc(&h->step_dev, sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
+    if ((e = cudaMalloc(&h->step_dev, 2 * sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
     if ((e = cudaMalloc(&h->colors, (size_t)kGraphSweeps * nchains)) != cudaSuccess) return bail(e, "cudaMalloc colors");
     if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess)
         return bail(e, "cudaEventCreate");
@@ -1142,6 +1170,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         if ((e = cudaMalloc(&h->m_cost, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cudaMalloc cost");
         if ((e = cudaMemset(h->m_cost, 0, sizeof(unsigned) * iota.size())) != cudaSuccess) return bail(e, "cost");
         if (const char *ev = getenv("TSB_DOM_ADAPT")) h->m_adapt = atoi(ev) != 0;
+        if (const char *ev = getenv("TSB_DOM_COLLAPSE")) h->collapse = atoi(ev) != 0;
         if (const char *ev = getenv("TSB_DOM_ORDER_EVERY")) h->m_order_every = std::max(1, atoi(ev));
     }
     for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
@@ -1322,6 +1351,7 @@ static int launch_resident(tsb_domino *h, int chain0, int n, uint64_t step0, uin
     c.W = h->W;
     c.step0 = step0;
     c.n_steps = n_steps;
+    c.collapse = h->collapse;
     const size_t items = (size_t)h->side * h->W;
     const int threads = (int)std::min<size_t>(kResThreads, (items + 31) / 32 * 32);
     const void *fn = h->tmode == 0 ? (const void *)domino_resident_kernel<0>
@@ -1345,13 +1375,13 @@ int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n
     }
     if (n_steps >= kGraphSweeps) {
         if ((rc = ensure_graph(h, chain0, n))) return rc;
-        set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        set_walk_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         TSB_CUDA(cudaGetLastError());
         for (; s + kGraphSweeps <= n_steps; s += kGraphSweeps) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
     }
     if (n_steps - s >= (uint64_t)kMK) {  // remainder: direct multi-sweep launches (step_dev = step0 + s)
-        if (s == 0) set_step_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
-        colors_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->seedinfo, h->step_dev, 0, h->colors);
+        if (s == 0) set_walk_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
+        colors_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
         TSB_CUDA(cudaGetLastError());
         for (uint64_t i = 0; s + kMK <= n_steps; s += kMK, i += kMK)
             if ((rc = launch_multi(h, chain0, n, i, h->stream))) return rc;
@@ -1417,6 +1447,12 @@ static int row_copy(tsb_domino *h, int chain, int r0, int nrows, void *dev, bool
 int tsb_domino_row_bytes(tsb_domino *h, int64_t *bytes) {
     if (!h || !bytes) return fail(TSB_E_VALUE, "null argument");
     *bytes = (int64_t)sizeof(uint2) * h->pitch;
+    return TSB_OK;
+}
+
+int tsb_domino_set_collapse(tsb_domino *h, int on) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    h->collapse = on ? 1 : 0;
     return TSB_OK;
 }
 

@@ -31,6 +31,7 @@ struct tsb_domino {
     int num_sms = 148;
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
     bool coupled = false, g_coupled = false;  // chains 2j, 2j+1 share seeds (CFTP pairs): share the coins
+    int collapse = 1, g_collapse = -1;  // skip sweeps followed by a sweep of the same colour (colors_kernel)
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;

@@ -35,7 +35,6 @@ class CopyPool {
     explicit CopyPool(int n) : n_(n) {
         for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
     }
-    int size() const { return n_; }
     // fn(part, nparts) on every pool thread (part 0 on the caller)
     void run(const std::function<void(int, int)> &fn) {
         {

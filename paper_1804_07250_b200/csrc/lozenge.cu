@@ -63,6 +63,7 @@ struct tsb_loz {
     int2 *mtiles = nullptr;  // tiles of the temporally blocked kernel (m_out-row bands)
     int nmtiles = 0;
     int m_K = 4, m_out = 8;
+    int collapse = 1, g_collapse = -1;  // run collapsing (TSB_LZ_COLLAPSE, tsb_loz_set_collapse)
     // height export scratch, allocated on first use (no cudaMalloc per call)
     int *hx_h = nullptr, *hx_flags = nullptr, *hx_off = nullptr;
     int4 *hx_rows = nullptr;
@@ -207,6 +208,7 @@ struct LzMCtx {
     int X, Y, W, pitch;
     int K, out_rows;
     uint64_t step;  // offset of this launch inside the graph replay
+    int collapse;   // skip sweeps followed by a sweep of the same class
 };
 
 // Temporal blocking: K sweeps per launch (graph replays), the domino
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
     const uint32_t *rA = c.src + (size_t)z * c.chain_words + (ptrdiff_t)x * c.pitch;
     const uint32_t *rB = rA + c.plane, *rC = rB + c.plane;
     Words2 A = ld2(rA, wa, ina, inb), B = ld2(rB, wa, ina, inb), C = ld2(rC, wa, ina, inb);
-    const uint64_t step0 = *c.step_dev + c.step;
+    const uint64_t step0 = c.step_dev[0] + c.step, walk_end = c.step_dev[1];
     int mycls;
     {
         const double coin = (double)(mix64(gkey + (step0 + (uint64_t)lane + 1ull) * kGold) >> 11) * 0x1p-53;
@@ -250,6 +252,11 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
 #pragma unroll 1
     for (int s = 0; s < c.K; ++s) {
         const int cls = __shfl_sync(0xffffffffu, mycls, s);
+        // run collapsing: heat-bath move (a rotateable star ends high iff
+        // u < p, lozenge.py:575-597) and same-class stars are disjoint, so
+        // within a run of one class only its last sweep decides
+        if (c.collapse && step0 + (uint64_t)s + 1ull < walk_end && __shfl_sync(0xffffffffu, mycls, s + 1) == cls)
+            continue;
         acs[k][lane] = make_uint4(A.a, A.b, C.a, C.b);
         __syncthreads();
         const uint4 m = k > 0 ? acs[k - 1][lane] : make_uint4(0u, 0u, 0u, 0u);  // A, C of row x-1
@@ -307,7 +314,10 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
     }
 }
 
-__global__ void lz_set_step(uint64_t *p, uint64_t v) { *p = v; }
+__global__ void lz_set_step(uint64_t *p, uint64_t v, uint64_t end) {  // p[0] = step, p[1] = end of the walk
+    p[0] = v;
+    p[1] = end;
+}
 __global__ void lz_advance_step(uint64_t *p, uint64_t by) { *p += by; }
 
 __device__ __forceinline__ bool tri_in(const uint8_t *t, int sx, int sy, int x, int y) {
@@ -671,6 +681,7 @@ int lz_launch_multi(tsb_loz *h, int chain0, int n, uint64_t step_off, cudaStream
     c.W = h->W;
     c.pitch = h->pitch;
     c.K = h->m_K;
+    c.collapse = h->collapse;
     c.out_rows = h->m_out;
     c.step = step_off;
     h->cur ^= 1;
@@ -699,7 +710,7 @@ int lz_launch_multi(tsb_loz *h, int chain0, int n, uint64_t step_off, cudaStream
 
 int lz_graph(tsb_loz *h, int chain0, int n) {
     if (h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur && h->g_tmode == h->tmode &&
-        h->g_t0 == h->t0)
+        h->g_t0 == h->t0 && h->g_collapse == h->collapse)
         return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
@@ -730,6 +741,7 @@ int lz_graph(tsb_loz *h, int chain0, int n) {
     h->g_cur = h->cur;
     h->g_tmode = h->tmode;
     h->g_t0 = h->t0;
+    h->g_collapse = h->collapse;
     return TSB_OK;
 }
 
@@ -1093,6 +1105,7 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
                 return bail(e, "smem attribute");
         cudaDeviceGetAttribute(&h->m_sms, cudaDevAttrMultiProcessorCount, h->device);
         if (const char *ev = getenv("TSB_LZ_DENSE")) h->m_dense = atoi(ev) ? 1 : 0;
+        if (const char *ev = getenv("TSB_LZ_COLLAPSE")) h->collapse = atoi(ev) != 0;
         if ((e = cudaFuncSetAttribute(lz_multi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kLzMSmem)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(lz_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1102,7 +1115,7 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
     if ((e = cudaMalloc(&h->seedinfo, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess) return bail(e, "seeds");
     if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess) return bail(e, "seeds");
     if ((e = cudaMalloc(&h->flag, 2 * sizeof(int))) != cudaSuccess) return bail(e, "flag");
-    if ((e = cudaMalloc(&h->step_dev, sizeof(uint64_t))) != cudaSuccess) return bail(e, "step");
+    if ((e = cudaMalloc(&h->step_dev, 2 * sizeof(uint64_t))) != cudaSuccess) return bail(e, "step");
     if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
     if ((e = cudaEventRecord(h->seed_ev, h->stream)) != cudaSuccess) return bail(e, "event");
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "create");
@@ -1225,12 +1238,12 @@ int tsb_loz_walk(tsb_loz *h, int chain0, int n, const uint64_t *seeds, uint64_t 
     uint64_t s = 0;
     if (n_steps >= 2 * kLzGraph) {
         if ((rc = lz_graph(h, chain0, n))) return rc;
-        lz_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        lz_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         TSB_CUDA(cudaGetLastError());
         for (; s + kLzGraph <= n_steps; s += kLzGraph) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
     }
     if (n_steps - s >= (uint64_t)h->m_K) {  // remainder: direct multi-sweep launches (step_dev = step0 + s)
-        if (s == 0) lz_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        if (s == 0) lz_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         TSB_CUDA(cudaGetLastError());
         for (uint64_t i = 0; s + h->m_K <= n_steps; s += h->m_K, i += h->m_K)
             if ((rc = lz_launch_multi(h, chain0, n, i, h->stream))) return rc;
@@ -1317,6 +1330,12 @@ int tsb_loz_extremal(tsb_loz *h, int chain_max, int chain_min, int ref_x, int re
     }
     if (rc) return rc;
     if (untileable) return fail(TSB_E_UNTILEABLE, "triangle domain is not tileable");
+    return TSB_OK;
+}
+
+int tsb_loz_set_collapse(tsb_loz *h, int on) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    h->collapse = on ? 1 : 0;
     return TSB_OK;
 }
 

@@ -55,6 +55,7 @@ struct tsb_sv {
     cudaGraphExec_t graph_exec = nullptr;
     int g_chain0 = -1, g_n = -1;
     uint64_t lut_version = 0, g_lut_version = ~0ull;
+    int collapse = 1, g_collapse = -1;  // run collapsing (TSB_SV_COLLAPSE, tsb_sv_set_collapse)
 };
 
 namespace tsb {
@@ -170,6 +171,7 @@ struct SvMCtx {
     size_t chain_words;
     int n, f, W, pitch;
     int K, out_rows;      // sweeps per launch, exact rows per tile (2*NW - 2K)
+    int collapse;         // skip sweeps followed by a sweep of the same class
     int stride, woff;     // column tiles: first word of tile x = x*stride + woff
     uint64_t step;        // offset of this launch inside the graph replay
     uint64_t lut[32];
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t step0 = *c.step_dev + c.step;
+    const uint64_t step0 = c.step_dev[0] + c.step, walk_end = c.step_dev[1];
     // class of sweep s is computed by lane s: min(int(u*4),3) = x >> 62
     const int mycls = (int)(mix64(gkey + (step0 + (uint64_t)lane + 1ull) * kGold) >> 62);
     const uint32_t *src = c.src + (size_t)z * c.chain_words;
@@ -233,6 +235,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
 #pragma unroll 1
     for (int s = 0; s < c.K; ++s) {
         const int cls = __shfl_sync(0xffffffffu, mycls, s);
+        // run collapsing: the move is a heat-bath update (after it a candidate
+        // is a local maximum iff u < p_high, whatever it was, sixvertex.py:
+        // 420-441) and within a run of one class nothing else moves, so only
+        // the run's last sweep decides (bit-identical; block-uniform skip)
+        if (c.collapse && step0 + (uint64_t)s + 1ull < walk_end && __shfl_sync(0xffffffffu, mycls, s + 1) == cls)
+            continue;
         const int pr = cls >> 1, pc = cls & 1;
         const int i = 2 * k + pr, R = r0 + i;
         uint32_t u[WPL], b[WPL], d[WPL];
@@ -349,7 +357,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
     }
 }
 
-__global__ void sv_set_step(uint64_t *p, uint64_t v) { *p = v; }
+__global__ void sv_set_step(uint64_t *p, uint64_t v, uint64_t end) {  // p[0] = step, p[1] = end of the walk
+    p[0] = v;
+    p[1] = end;
+}
 __global__ void sv_advance_step(uint64_t *p, uint64_t by) { *p += by; }
 
 // int32 heights (count, f, f) -> bits; validates |dh| == 1 across every edge.
@@ -511,7 +522,7 @@ void sv_multi_config(tsb_sv *h) {
         h->m_gx = (h->W + h->m_stride - 1) / h->m_stride;
     }
     int nw = 16, K = 8;
-    if (const char *e = getenv("TSB_SV_NW")) nw = atoi(e) == 16 ? 16 : 8;
+    if (const char *e = getenv("TSB_SV_NW")) nw = atoi(e) == 16 ? 16 : atoi(e) == 15 ? 15 : 8;
     if (const char *e = getenv("TSB_SV_K")) {
         K = atoi(e);
         h->m_k_fixed = true;
@@ -580,6 +591,7 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
     c.W = h->W;
     c.pitch = h->pitch;
     c.K = sv_k(h, n);
+    c.collapse = h->collapse;
     c.out_rows = 2 * h->m_nw - 2 * c.K;
     c.stride = h->m_stride;
     c.woff = h->m_woff;
@@ -602,6 +614,9 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
         case 116: return sv_launch_multi_t<1, 16>(cfg, c, h->m_sms);
         case 216: return sv_launch_multi_t<2, 16>(cfg, c, h->m_sms);
         case 316: return sv_launch_multi_t<3, 16>(cfg, c, h->m_sms);
+        case 315: return sv_launch_multi_t<3, 15>(cfg, c, h->m_sms);
+        case 215: return sv_launch_multi_t<2, 15>(cfg, c, h->m_sms);
+        case 115: return sv_launch_multi_t<1, 15>(cfg, c, h->m_sms);
         default: return sv_launch_multi_t<4, 16>(cfg, c, h->m_sms);
     }
 }
@@ -609,7 +624,9 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
 // Graph of kSvGraphSweeps sweeps: an even number of out-of-place launches
 // (bits -> bits2 -> bits ...), then step += kSvGraphSweeps.
 static int sv_ensure_graph(tsb_sv *h, int chain0, int n) {
-    if (h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_lut_version == h->lut_version) return TSB_OK;
+    if (h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_lut_version == h->lut_version &&
+        h->g_collapse == h->collapse)
+        return TSB_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
@@ -638,6 +655,7 @@ static int sv_ensure_graph(tsb_sv *h, int chain0, int n) {
     h->g_chain0 = chain0;
     h->g_n = n;
     h->g_lut_version = h->lut_version;
+    h->g_collapse = h->collapse;
     return TSB_OK;
 }
 
@@ -793,9 +811,10 @@ int tsb_sv_create(int device, int n, int nchains, tsb_sv **out) {
     if (e == cudaSuccess) e = cudaEventRecord(h->seed_ev, h->stream);
     if (e == cudaSuccess) e = cudaMalloc(&h->bits2, sizeof(uint32_t) * h->chain_words * nchains);
     if (e == cudaSuccess) e = cudaMemset(h->bits2, 0, sizeof(uint32_t) * h->chain_words * nchains);
-    if (e == cudaSuccess) e = cudaMalloc(&h->step_dev, sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&h->step_dev, 2 * sizeof(uint64_t));
     for (int i = 0; i < 32; ++i) h->lut[i] = 1ull << 52;
     sv_multi_config(h);
+    if (const char *ev = getenv("TSB_SV_COLLAPSE")) h->collapse = atoi(ev) != 0;
     if (e != cudaSuccess) {
         int code = cuda_fail(e, "tsb_sv_create");
         tsb_sv_destroy(h);
@@ -894,14 +913,14 @@ static int sv_walk_impl(tsb_sv *h, int chain0, int n, const uint64_t *seeds, uin
     const uint64_t replays = class_override < 0 ? n_steps / kSvGraphSweeps : 0;
     if (replays) {
         if ((rc = sv_ensure_graph(h, chain0, n))) return rc;
-        sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         for (uint64_t r = 0; r < replays; ++r) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
         done = replays * kSvGraphSweeps;
     }
     const uint64_t Kn = (uint64_t)sv_k(h, n);
     if (class_override < 0 && n_steps - done >= Kn) {
         // remainder: direct multi-sweep launches bits -> bits2 -> ..., step_dev = step0 + done
-        if (done == 0) sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0);
+        if (done == 0) sv_set_step<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         int launches = 0;
         for (uint64_t i = 0; done + Kn <= n_steps; done += Kn, i += Kn, ++launches)
             if ((rc = sv_launch_multi(h, chain0, n, i, (launches & 1) ? h->bits2 : h->bits,
@@ -982,6 +1001,12 @@ int tsb_sv_extremal(tsb_sv *h, const int32_t *ring, int chain_max, int chain_min
         if (dst) std::copy(g.begin(), g.end(), dst);
     }
     cudaFree(dg);
+    return TSB_OK;
+}
+
+int tsb_sv_set_collapse(tsb_sv *h, int on) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    h->collapse = on ? 1 : 0;
     return TSB_OK;
 }
 

@@ -479,6 +479,10 @@ class LozengeHandle:
     def set_stream(self, stream_ptr: int):
         _native.check(_native.lib().tsb_loz_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
 
+    def set_collapse(self, on: bool):
+        """Class-run collapsing (tsb_loz_set_collapse); bit-identical results."""
+        _native.check(_native.lib().tsb_loz_set_collapse(self._h, int(bool(on))))
+
     def set_p_up(self, p_up: np.ndarray):
         if self._p_ref is p_up:
             return

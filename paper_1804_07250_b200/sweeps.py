@@ -217,6 +217,11 @@ class DominoHandle:
     def set_stream(self, stream_ptr: int):
         _native.check(_native.lib().tsb_domino_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
 
+    def set_collapse(self, on: bool):
+        """Run collapsing (tsb_domino_set_collapse): skip sweeps followed by a
+        sweep of the same colour; bit-identical results."""
+        _native.check(_native.lib().tsb_domino_set_collapse(self._h, int(bool(on))))
+
     def set_p_up(self, p_up: np.ndarray):
         if self._p_up_ref is p_up:
             return
