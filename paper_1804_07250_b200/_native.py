@@ -177,6 +177,8 @@ def lib() -> ctypes.CDLL:
                         raise RuntimeError(f"libtsb.so is missing and could not be built: {exc}")
             L = ctypes.CDLL(path or LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if path is not None and not hasattr(L, name):
+                    continue  # an older A/B build may lack newer entry points
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
