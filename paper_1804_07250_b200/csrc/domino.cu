@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include <cub/block/block_reduce.cuh>
@@ -63,7 +64,32 @@ struct SweepCtx {
     int color_override;  // -1: colour from the global coin (direct launches)
     const int *order;    // multi-sweep adaptive order: canonical index of the tile of block b (tiles permuted)
     unsigned *cost;      // multi-sweep: per-tile block duration in cycles (null: not measured)
+    // compacted walks (walk_compact): executed sweeps of chain z are
+    // xlist[z * xpitch + j], j < xcnt[z] = (step - step_dev[0]) | colour << 31;
+    // launch sweep s takes entry *xbase + step + s (null: colour table)
+    const uint32_t *xlist;
+    const int *xcnt;
+    const uint64_t *xbase;
+    int xpitch;
 };
+
+// Step and colour of sweep s of a multi-sweep launch for chain z; false when
+// the sweep is not executed (a collapsed run, or past the chain's list).
+__device__ __forceinline__ bool sweep_of(const SweepCtx &c, int z, int s, uint64_t step0, uint64_t *step,
+                                         int *color) {
+    if (c.xlist) {
+        const uint64_t j = *c.xbase + c.step + (uint64_t)s;
+        if (j >= (uint64_t)c.xcnt[z]) return false;
+        const uint32_t e = c.xlist[(size_t)z * c.xpitch + j];
+        *step = c.step_dev[0] + (e & 0x7FFFFFFFu);
+        *color = (int)(e >> 31);
+        return true;
+    }
+    const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
+    *step = step0 + (uint64_t)s;
+    *color = ci & 1;
+    return !(ci & 2);
+}
 
 // One sweep, one block per non-empty tile of kTileRows x 62 words (512
 // threads).  Warp k owns row r = r0+k; each lane owns two adjacent words
@@ -201,10 +227,9 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
-        const uint64_t step = step0 + (uint64_t)s;
-        const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
-        if (ci & 2) continue;  // collapsed run: block-uniform
-        const int color = ci & 1;
+        uint64_t step;
+        int color;
+        if (!sweep_of(c, z, s, step0, &step, &color)) continue;  // block-uniform
         vs[k][lane] = make_uint2(cur.x, cur.z);
         __syncthreads();
         uint32_t vua = 0u, vub = 0u;
@@ -370,10 +395,9 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
-        const uint64_t step = step0 + (uint64_t)s;
-        const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
-        if (ci & 2) continue;  // collapsed run: block-uniform
-        const int color = ci & 1;
+        uint64_t step;
+        int color;
+        if (!sweep_of(c, z, s, step0, &step, &color)) continue;  // block-uniform
         vs[k][lane] = cur.x;
         __syncthreads();
         const uint32_t vu = k > 0 ? vs[k - 1][lane] : 0u;
@@ -562,10 +586,9 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
-        const uint64_t step = step0 + (uint64_t)s;
-        const int ci = c.colors[zt * kGraphSweeps + (int)c.step + s];
-        if (ci & 2) continue;  // collapsed run: block-uniform
-        const int color = ci & 1;
+        uint64_t step;
+        int color;
+        if (!sweep_of(c, zt, s, step0, &step, &color)) continue;  // block-uniform
         vs[0][k][lane] = ct.x;
         vs[1][k][lane] = cb.x;
         __syncthreads();
@@ -737,10 +760,12 @@ int check_range(tsb_domino *h, int chain0, int n) {
 
 int push_seeds(tsb_domino *h, int n, const uint64_t *seeds) {
     TSB_CUDA(cudaEventSynchronize(h->seed_ev));  // staging free again
+    if ((int)h->gkeys.size() < n) h->gkeys.resize(n);
     for (int i = 0; i < n; ++i) {
         const uint64_t b = family_base(seeds[i]);
         h->seed_pinned[2 * i] = b;
         h->seed_pinned[2 * i + 1] = global_key(b);
+        h->gkeys[i] = global_key(b);
     }
     TSB_CUDA(cudaMemcpyAsync(h->seedinfo, h->seed_pinned, sizeof(uint64_t) * 2 * n,
                              cudaMemcpyHostToDevice, h->stream));
@@ -769,6 +794,10 @@ int launch_sweep(tsb_domino *h, int chain0, int n, uint64_t step, int color_over
     c.color_override = color_override;
     c.order = nullptr;
     c.cost = nullptr;
+    c.xlist = nullptr;
+    c.xcnt = nullptr;
+    c.xbase = nullptr;
+    c.xpitch = 0;
     h->cur ^= 1;
     if (h->ntiles == 0) return TSB_OK;
     cudaLaunchConfig_t cfg = {};
@@ -810,7 +839,7 @@ static bool adaptive_order(const tsb_domino *h, int n) {
 }
 
 // kMK sweeps (temporally blocked) of chains [chain0, chain0+n); graph mode only.
-int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream_t stream) {
+int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream_t stream, bool compact) {
     SweepCtx c;
     const size_t off = (size_t)chain0 * h->chain_stride + h->pitch + kPad;
     c.src = h->buf[h->cur] + off;
@@ -828,6 +857,10 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     c.pitch = h->pitch;
     c.step = step_off;
     c.color_override = -1;
+    c.xlist = compact ? h->xlist : nullptr;
+    c.xcnt = compact ? h->xcnt : nullptr;
+    c.xbase = compact ? h->step_dev + 2 : nullptr;
+    c.xpitch = (int)h->xpitch;
     const bool adapt = adaptive_order(h, n);
     // adaptive order over the launched window: indices relative to its first tile
     c.order = adapt ? h->m_order + h->win_m0 : nullptr;
@@ -963,8 +996,9 @@ __global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *co
 // started) followed by `step += kGraphSweeps`; long walks replay it, which
 // removes the per-launch host overhead (the kernels read the step base from
 // device memory).
-int ensure_graph(tsb_domino *h, int chain0, int n) {
+int ensure_graph(tsb_domino *h, int chain0, int n, bool compact) {
     const bool same = h->graph_exec && h->g_chain0 == chain0 && h->g_n == n && h->g_cur == h->cur &&
+                      h->g_compact == (int)compact &&
                       h->g_tmode == h->tmode && h->g_t0 == h->t0 && h->g_t1 == h->t1 &&
                       h->g_win0 == h->win_t0 && h->g_winn == h->win_tn && h->g_winm == h->win_m0 &&
                       h->g_tail == h->graph_tail && h->g_coupled == h->coupled && h->g_collapse == h->collapse;
@@ -977,13 +1011,19 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     cudaGraph_t g = nullptr;
     TSB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = TSB_OK;
-    colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
+    // compact replays take the next kGraphSweeps entries of the executed-sweep
+    // lists (step_dev[2] advances); colour-table replays the next kGraphSweeps
+    // steps (step_dev[0] advances)
+    uint64_t *counter = compact ? h->step_dev + 2 : h->step_dev;
+    if (!compact)
+        colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
-    for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i) rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream);
+    for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i)
+        rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream, compact);
     if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost + h->win_m0, h->mtiles + h->win_m0, h->win_mn,
-                                                          h->step_dev, h->m_order_every, h->m_order + h->win_m0,
+                                                          counter, h->m_order_every, h->m_order + h->win_m0,
                                                           h->m_perm + h->win_m0);
-    advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(h->step_dev, (uint64_t)kGraphSweeps);
+    advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(counter, (uint64_t)kGraphSweeps);
     if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) {
@@ -1009,6 +1049,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n) {
     h->g_tail = h->graph_tail;
     h->g_coupled = h->coupled;
     h->g_collapse = h->collapse;
+    h->g_compact = (int)compact;
     return TSB_OK;
 }
 
@@ -1071,7 +1112,7 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     if ((e = cudaMallocHost(&h->seed_pinned, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
         return bail(e, "cudaMallocHost seeds");
     if ((e = cudaMalloc(&h->bad, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc flag");
-    if ((e = cudaMalloc(&h->step_dev, 2 * sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
+    if ((e = cudaMalloc(&h->step_dev, 3 * sizeof(uint64_t))) != cudaSuccess) return bail(e, "cudaMalloc step");
     if ((e = cudaMalloc(&h->colors, (size_t)kGraphSweeps * nchains)) != cudaSuccess) return bail(e, "cudaMalloc colors");
     if ((e = cudaEventCreateWithFlags(&h->seed_ev, cudaEventDisableTiming)) != cudaSuccess)
         return bail(e, "cudaEventCreate");
@@ -1213,6 +1254,12 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaFree(h->dom);
     cudaFree(h->fbits);
     cudaFree(h->range);
+    cudaFree(h->xlist);
+    cudaFree(h->xcnt);
+    for (int i = 0; i < 2; ++i) {
+        if (h->xpin[i]) cudaFreeHost(h->xpin[i]);
+        if (h->xev[i]) cudaEventDestroy(h->xev[i]);
+    }
     cudaFree(h->hx_h);
     cudaFree(h->hx_flags);
     cudaFree(h->hx_rows);
@@ -1375,6 +1422,96 @@ static int launch_resident(tsb_domino *h, int chain0, int n, uint64_t step0, uin
     return TSB_OK;
 }
 
+__global__ void set_segment_kernel(uint64_t *step_dev, uint64_t step) {
+    step_dev[0] = step;  // base of the executed-sweep offsets
+    step_dev[2] = 0;     // list cursor of the replays
+}
+
+// Executed-sweep lists of a walk segment (run collapsing, host side): sweep i
+// of the segment is executed unless sweep i+1 of the same walk has the same
+// colour (colors_kernel explains why that is exact).  Entry = i | colour << 31.
+static int build_lists(tsb_domino *h, int n, uint64_t seg_step, uint64_t len, bool walk_end, uint32_t *list,
+                       int *cnt) {
+    const size_t pitch = h->xpitch;
+    auto one = [&](int z) {
+        const uint64_t g = h->gkeys[z];
+        uint32_t *o = list + (size_t)z * pitch;
+        int m = 0;
+        int col = (int)(mix64(g + (seg_step + 1ull) * kGold) >> 63);
+        for (uint64_t i = 0; i < len; ++i) {
+            const bool last = i + 1 == len;
+            const int nxt = (last && walk_end) ? -1 : (int)(mix64(g + (seg_step + i + 2ull) * kGold) >> 63);
+            if (nxt != col) o[m++] = (uint32_t)i | ((uint32_t)col << 31);
+            col = nxt;
+        }
+        cnt[z] = m;
+    };
+    host_parallel_for(n, [&](int z) {
+        if (h->coupled && (z & 1)) return;  // CFTP pairs share their seeds: the pair's second list is a copy
+        one(z);
+    });
+    if (h->coupled)
+        for (int z = 1; z < n; z += 2) {
+            std::memcpy(list + (size_t)z * pitch, list + (size_t)(z - 1) * pitch, sizeof(uint32_t) * cnt[z - 1]);
+            cnt[z] = cnt[z - 1];
+        }
+    return TSB_OK;
+}
+
+constexpr uint64_t kSegSweeps = 16384;  // raw sweeps per list segment
+
+static int xlist_alloc(tsb_domino *h) {
+    if (h->xlist) return TSB_OK;
+    h->xpitch = kSegSweeps;
+    const size_t entries = (size_t)h->nchains * h->xpitch;
+    TSB_CUDA(cudaMalloc(&h->xlist, sizeof(uint32_t) * entries));
+    TSB_CUDA(cudaMalloc(&h->xcnt, sizeof(int) * h->nchains));
+    for (int i = 0; i < 2; ++i) {
+        TSB_CUDA(cudaMallocHost(&h->xpin[i], sizeof(uint32_t) * entries + sizeof(int) * h->nchains));
+        TSB_CUDA(cudaEventCreateWithFlags(&h->xev[i], cudaEventDisableTiming));
+        TSB_CUDA(cudaEventRecord(h->xev[i], h->stream));
+    }
+    return TSB_OK;
+}
+
+// Run-collapsed walk: per segment, the executed sweeps of every chain are
+// listed on the host and uploaded; graph replays then sweep kGraphSweeps
+// listed sweeps each (two per multi-sweep launch) and the remainder runs as
+// direct launches.  A launch past a chain's list copies its tiles, so every
+// chain ends each segment in the canonical buffer.
+static int walk_compact(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps) {
+    int rc = xlist_alloc(h);
+    if (rc) return rc;
+    const int cur0 = h->cur;
+    for (uint64_t seg = 0; seg < n_steps; seg += kSegSweeps) {
+        const uint64_t len = std::min<uint64_t>(kSegSweeps, n_steps - seg);
+        const int slot = h->xslot;
+        h->xslot ^= 1;
+        TSB_CUDA(cudaEventSynchronize(h->xev[slot]));  // the slot's previous upload has been consumed
+        uint32_t *list = h->xpin[slot];
+        int *cnt = reinterpret_cast<int *>(list + (size_t)h->nchains * h->xpitch);
+        if ((rc = build_lists(h, n, step0 + seg, len, seg + len == n_steps, list, cnt))) return rc;
+        int maxe = 0;
+        for (int z = 0; z < n; ++z) maxe = std::max(maxe, cnt[z]);
+        TSB_CUDA(cudaMemcpy2DAsync(h->xlist, sizeof(uint32_t) * h->xpitch, list, sizeof(uint32_t) * h->xpitch,
+                                   sizeof(uint32_t) * std::max(1, maxe), n, cudaMemcpyHostToDevice, h->stream));
+        TSB_CUDA(cudaMemcpyAsync(h->xcnt, cnt, sizeof(int) * n, cudaMemcpyHostToDevice, h->stream));
+        TSB_CUDA(cudaEventRecord(h->xev[slot], h->stream));
+        set_segment_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0 + seg);
+        TSB_CUDA(cudaGetLastError());
+        const int replays = maxe / kGraphSweeps;
+        if (replays) {
+            if ((rc = ensure_graph(h, chain0, n, true))) return rc;
+            for (int r = 0; r < replays; ++r) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
+        }
+        int launches = (maxe - replays * kGraphSweeps + kMK - 1) / kMK;
+        launches += launches & 1;  // even: the chains end where they started
+        for (int i = 0; i < launches; ++i)
+            if ((rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->stream, true))) return rc;
+    }
+    return settle(h, chain0, n, cur0);
+}
+
 int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n_steps) {
     int rc;
     const int cur0 = h->cur;
@@ -1382,8 +1519,10 @@ int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n
     if (n_steps >= 2) {
         if (const size_t smem = resident_smem(h, n)) return launch_resident(h, chain0, n, step0, n_steps, smem);
     }
+    if (h->collapse && !h->strip && n_steps >= 2 && (int)h->gkeys.size() >= n)
+        return walk_compact(h, chain0, n, step0, n_steps);
     if (n_steps >= kGraphSweeps) {
-        if ((rc = ensure_graph(h, chain0, n))) return rc;
+        if ((rc = ensure_graph(h, chain0, n, false))) return rc;
         set_walk_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
         TSB_CUDA(cudaGetLastError());
         for (; s + kGraphSweeps <= n_steps; s += kGraphSweeps) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
@@ -1393,7 +1532,7 @@ int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n
         colors_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
         TSB_CUDA(cudaGetLastError());
         for (uint64_t i = 0; s + kMK <= n_steps; s += kMK, i += kMK)
-            if ((rc = launch_multi(h, chain0, n, i, h->stream))) return rc;
+            if ((rc = launch_multi(h, chain0, n, i, h->stream, false))) return rc;
     }
     for (; s < n_steps; ++s)
         if ((rc = launch_sweep(h, chain0, n, step0 + s, -1, h->stream, nullptr))) return rc;

@@ -32,6 +32,15 @@ struct tsb_domino {
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
     bool coupled = false, g_coupled = false;  // chains 2j, 2j+1 share seeds (CFTP pairs): share the coins
     int collapse = 1, g_collapse = -1;  // skip sweeps followed by a sweep of the same colour (colors_kernel)
+    int g_compact = -1;
+    // run-collapsed walks (walk_compact): executed-sweep lists per chain
+    std::vector<uint64_t> gkeys;  // host copies of the pushed chains' global keys
+    uint32_t *xlist = nullptr;    // device [nchains][xpitch]
+    int *xcnt = nullptr;          // device [nchains]
+    size_t xpitch = 0;
+    uint32_t *xpin[2] = {nullptr, nullptr};  // pinned staging: lists then counts
+    cudaEvent_t xev[2] = {nullptr, nullptr};
+    int xslot = 0;
     int tmode = 0;
     uint64_t t0 = 1ull << 52, t1 = 1ull << 52;
     uint64_t *tgrid = nullptr;

@@ -93,13 +93,17 @@ Stage &stage() {
     return s;
 }
 
-int stage_init(Stage &s) {
-    int dev = 0;
-    TSB_CUDA(cudaGetDevice(&dev));
+void pool_init(Stage &s) {
     if (!s.pool) {
         const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
         s.pool = new CopyPool((int)std::min(8u, std::max(1u, hc / 2)));
     }
+}
+
+int stage_init(Stage &s) {
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    pool_init(s);
     if (s.device != dev) {  // (re)create slots and events on the current device
         for (int i = 0; i < kSlots; ++i) {
             if (s.slot[i]) {
@@ -137,6 +141,19 @@ bool pinned(const void *p) {
 }
 
 }  // namespace
+
+void host_parallel_for(int n, const std::function<void(int)> &fn) {
+    if (n <= 1) {
+        if (n == 1) fn(0);
+        return;
+    }
+    Stage &s = stage();
+    std::lock_guard<std::mutex> g(s.mu);
+    pool_init(s);
+    s.pool->run([&](int p, int np) {
+        for (int i = p; i < n; i += np) fn(i);
+    });
+}
 
 int staged_h2d(void *dev, const void *src, size_t bytes, cudaStream_t stream) {
     if (bytes < kDirectBelow || pinned(src)) {

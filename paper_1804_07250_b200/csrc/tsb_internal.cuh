@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <functional>
 #include <string>
 
 #include "../../include/tsb.h"
@@ -109,6 +110,8 @@ __device__ __forceinline__ int block_exclusive_sum(int v, int *sh) {
 // d2h returns with the copy complete
 int staged_h2d(void *dev, const void *src, size_t bytes, cudaStream_t stream);
 int staged_d2h(void *dst, const void *dev, size_t bytes, cudaStream_t stream);
+// fn(i) for i in [0, n) on the staging engine's host threads
+void host_parallel_for(int n, const std::function<void(int)> &fn);
 
 void set_error(const char *fmt, ...);
 int fail(int code, const char *fmt, ...);
