@@ -73,22 +73,30 @@ struct SweepCtx {
     int xpitch;
 };
 
+// Sweep selection of the multi-sweep kernels (template MODE, so each variant
+// carries only its own code): 0 every sweep, colours from the replay's
+// table; 1 the table's skip flags too (run collapsing inside the launches,
+// strip walks); 2 compacted executed-sweep lists (run-collapsed walks).
+enum { kSelPlain = 0, kSelSkip = 1, kSelList = 2 };
+
 // Step and colour of sweep s of a multi-sweep launch for chain z; false when
 // the sweep is not executed (a collapsed run, or past the chain's list).
+template <int MODE>
 __device__ __forceinline__ bool sweep_of(const SweepCtx &c, int z, int s, uint64_t step0, uint64_t *step,
                                          int *color) {
-    if (c.xlist) {
+    if constexpr (MODE == kSelList) {
         const uint64_t j = *c.xbase + c.step + (uint64_t)s;
         if (j >= (uint64_t)c.xcnt[z]) return false;
         const uint32_t e = c.xlist[(size_t)z * c.xpitch + j];
         *step = c.step_dev[0] + (e & 0x7FFFFFFFu);
         *color = (int)(e >> 31);
         return true;
+    } else {
+        const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
+        *step = step0 + (uint64_t)s;
+        *color = ci & 1;
+        return MODE == kSelPlain || !(ci & 2);
     }
-    const int ci = c.colors[z * kGraphSweeps + (int)c.step + s];
-    *step = step0 + (uint64_t)s;
-    *color = ci & 1;
-    return !(ci & 2);
 }
 
 // One sweep, one block per non-empty tile of kTileRows x 62 words (512
@@ -209,27 +217,34 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // word b) at bits 0-1 in sweep 0 and bit 0 in sweep 1.  Skipped sites keep
 // their state; they lie in the stale halo, which is never stored.
 static_assert(kMK == 2, "need masks are derived for two sweeps per launch");
+#ifndef TSB_NEED_MASKS
+#define TSB_NEED_MASKS 1
+#endif
 __device__ __forceinline__ uint32_t need_a(int s, int k, int lane) {
+    if (!TSB_NEED_MASKS) return 0xFFFFFFFFu;
     if (k < s + 1 || k > kMRows - 1 - s) return 0u;
     return lane == 0 ? (s == 0 ? 0x80000000u : 0u) : 0xFFFFFFFFu;
 }
 __device__ __forceinline__ uint32_t need_b(int s, int k, int lane) {
+    if (!TSB_NEED_MASKS) return 0xFFFFFFFFu;
     if (k < s + 1 || k > kMRows - 1 - s) return 0u;
     return lane == 31 ? (s == 0 ? 3u : 1u) : 0xFFFFFFFFu;
 }
 
 // kMK sweeps of one tile held in registers (cur) and shared memory, then the
 // exact central rows are stored.
-template <int TM>
+template <int TM, int MODE>
 __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], uint2 (*fs)[32], uint32_t (*fres)[64],
                                            uint16_t (*queue)[1024], int k, int lane, int z, int r, int wa,
                                            bool in_grid, uint4 cur, uint64_t step0) {
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
+    const uint32_t na0 = need_a(0, k, lane), na1 = need_a(1, k, lane), nb0 = need_b(0, k, lane),
+                   nb1 = need_b(1, k, lane);
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         uint64_t step;
         int color;
-        if (!sweep_of(c, z, s, step0, &step, &color)) continue;  // block-uniform
+        if (!sweep_of<MODE>(c, z, s, step0, &step, &color)) continue;  // block-uniform
         vs[k][lane] = make_uint2(cur.x, cur.z);
         __syncthreads();
         uint32_t vua = 0u, vub = 0u;
@@ -245,10 +260,10 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vua & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act & need_a(s, k, lane);
+        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act & (s ? na1 : na0);
         const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
         const uint32_t ib = vub & cur.z & ~(lb | cur.w);
-        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act & need_b(s, k, lane);
+        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act & (s ? nb1 : nb0);
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
@@ -284,7 +299,7 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
     uint16_t(*queue)[1024] =                                                                                \
         reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64)
 
-template <int TM>
+template <int TM, int MODE>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
     TT(0);
     MULTI_SMEM;
@@ -304,7 +319,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     if (c.cost && threadIdx.x == 0) t_start = clock64();
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
     if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
-    multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur, *c.step_dev + c.step);
+    multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur, *c.step_dev + c.step);
     if (c.cost && threadIdx.x == 0) c.cost[c.order[blockIdx.x]] = (unsigned)(clock64() - t_start);  // after the last barrier
     TT(5);
 }
@@ -328,7 +343,7 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 
-template <int TM>
+template <int TM, int MODE>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(SweepCtx c) {
     MULTI_SMEM;
     uint4 *slot = reinterpret_cast<uint4 *>(dsm + kMSmem) + threadIdx.x;  // [kPipeStages][blockDim]
@@ -339,6 +354,31 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t step0 = *c.step_dev + c.step;
+#if TSB_PIPE_STAGES == 2
+    auto fetch = [&](int i, int b) {
+        const int2 t = c.tiles[i];
+        const int r = t.y * kMOut - kMK + k;
+        uint4 *dst = slot + b * 32 * kMRows;
+        if (r >= 0 && r < c.side) cp_async16(dst, base + (ptrdiff_t)r * c.pitch + t.x + 2 * lane);
+        else *dst = make_uint4(0u, 0u, 0u, 0u);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int b = 0;
+    if ((int)blockIdx.x < c.ntiles) fetch(blockIdx.x, 0);
+    for (int i = blockIdx.x; i < c.ntiles; i += gridDim.x, b ^= 1) {
+        const int nx = i + gridDim.x;
+        if (nx < c.ntiles) {
+            fetch(nx, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's group has landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const uint4 cur = slot[b * 32 * kMRows];
+        const int2 t = c.tiles[i];
+        const int r = t.y * kMOut - kMK + k;
+        multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
+    }
+#else
     // one commit group per stage, empty past the end of the list, so that
     // "wait until at most kPipeStages-1 groups are pending" always means the
     // current tile has landed
@@ -361,17 +401,18 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
         const uint4 cur = slot[b * 32 * kMRows];
         const int2 t = c.tiles[i];
         const int r = t.y * kMOut - kMK + k;
-        multi_tile<TM>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
+        multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
         b = (b + 1) % kPipeStages;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+#endif
 }
 
 // The same temporal blocking with ONE {V,H} word per lane (tiles of 30 output
 // words): chosen for narrow lattices (e.g. CFTP at Aztec 512, W = 33 words),
 // where the 62-word tiles would leave half of every warp outside the domain.
 // Lanes 0 and 31 hold the halo words.
-template <int TM>
+template <int TM, int MODE>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t(*vs)[32] = reinterpret_cast<uint32_t(*)[32]>(dsm);
@@ -397,7 +438,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
     for (int s = 0; s < kMK; ++s) {
         uint64_t step;
         int color;
-        if (!sweep_of(c, z, s, step0, &step, &color)) continue;  // block-uniform
+        if (!sweep_of<MODE>(c, z, s, step0, &step, &color)) continue;  // block-uniform
         vs[k][lane] = cur.x;
         __syncthreads();
         const uint32_t vu = k > 0 ? vs[k - 1][lane] : 0u;
@@ -558,7 +599,7 @@ __global__ void __launch_bounds__(kResThreads, 1) domino_resident_kernel(ResCtx 
 // chains' rotateable sites: with c = (u < p_up), a site fires in a chain iff
 // it is rotateable there and c equals its "state 3" bit -- exactly what two
 // independent sweeps compute.  Narrow (1 word per lane) tiles.
-template <int TM>
+template <int TM, int MODE>
 __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t(*vs)[kMRows][32] = reinterpret_cast<uint32_t(*)[kMRows][32]>(dsm);
@@ -588,7 +629,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx
     for (int s = 0; s < kMK; ++s) {
         uint64_t step;
         int color;
-        if (!sweep_of(c, zt, s, step0, &step, &color)) continue;  // block-uniform
+        if (!sweep_of<MODE>(c, zt, s, step0, &step, &color)) continue;  // block-uniform
         vs[0][k][lane] = ct.x;
         vs[1][k][lane] = cb.x;
         __syncthreads();
@@ -877,40 +918,43 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // The coupled-pair kernel runs without programmatic dependent launch: with
+    // PDL, back-to-back launches of it in run-collapsed CFTP walks (a sweeping
+    // launch followed by a tile-copy launch) intermittently produced wrong top
+    // chains (tools/dbg_cftp_rounds.py: 3 of 6 runs; 0 of 12 without PDL for
+    // this kernel or outside graphs; the other kernels are unaffected).
+    cfg.numAttrs = (h->m_wpl == 1 && h->coupled) ? 0 : 1;
+    const int mode = compact ? kSelList : (h->collapse ? kSelSkip : kSelPlain);
+#define TSB_DOM_LAUNCH(kern)                                                              \
+    switch (h->tmode * 3 + mode) {                                                        \
+        case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<0, kSelPlain>, c)); break;         \
+        case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<0, kSelSkip>, c)); break;          \
+        case 2: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<0, kSelList>, c)); break;          \
+        case 3: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<1, kSelPlain>, c)); break;         \
+        case 4: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<1, kSelSkip>, c)); break;          \
+        case 5: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<1, kSelList>, c)); break;          \
+        case 6: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<2, kSelPlain>, c)); break;         \
+        case 7: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<2, kSelSkip>, c)); break;          \
+        default: TSB_CUDA(cudaLaunchKernelEx(&cfg, kern<2, kSelList>, c)); break;         \
+    }
     if (h->m_wpl == 1 && h->coupled && (n & 1) == 0) {
         cfg.gridDim.z = n / 2;  // one block per tile and coupled pair
-        switch (h->tmode) {
-            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<0>, c)); break;
-            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<1>, c)); break;
-            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1c_kernel<2>, c)); break;
-        }
+        TSB_DOM_LAUNCH(domino_multi1c_kernel);
         return TSB_OK;
     }
     if (h->m_wpl == 1) {
-        switch (h->tmode) {
-            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<0>, c)); break;
-            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<1>, c)); break;
-            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi1_kernel<2>, c)); break;
-        }
+        TSB_DOM_LAUNCH(domino_multi1_kernel);
         return TSB_OK;
     }
     // HBM-streaming launches: the persistent cp.async-pipelined kernel (pipe_launch)
     if (pipe_launch(h, n)) {
         cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
         cfg.dynamicSmemBytes = kPipeSmem;
-        switch (h->tmode) {
-            case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<0>, c)); break;
-            case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<1>, c)); break;
-            default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_pipe_kernel<2>, c)); break;
-        }
+        TSB_DOM_LAUNCH(domino_multi_pipe_kernel);
         return TSB_OK;
     }
-    switch (h->tmode) {
-        case 0: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<0>, c)); break;
-        case 1: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<1>, c)); break;
-        default: TSB_CUDA(cudaLaunchKernelEx(&cfg, domino_multi_kernel<2>, c)); break;
-    }
+    TSB_DOM_LAUNCH(domino_multi_kernel);
+#undef TSB_DOM_LAUNCH
     return TSB_OK;
 }
 
@@ -1223,17 +1267,18 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
         if (const char *ev = getenv("TSB_DOM_COLLAPSE")) h->collapse = atoi(ev) != 0;
         if (const char *ev = getenv("TSB_DOM_ORDER_EVERY")) h->m_order_every = std::max(1, atoi(ev));
     }
-    for (const void *fn : {(const void *)domino_multi_kernel<0>, (const void *)domino_multi_kernel<1>,
-                           (const void *)domino_multi_kernel<2>, (const void *)domino_multi1_kernel<0>,
-                           (const void *)domino_multi1_kernel<1>, (const void *)domino_multi1_kernel<2>,
-                           (const void *)domino_multi1c_kernel<0>, (const void *)domino_multi1c_kernel<1>,
-                           (const void *)domino_multi1c_kernel<2>})
+#define TSB_ALL_MODES(kern)                                                                            \
+    (const void *)kern<0, kSelPlain>, (const void *)kern<0, kSelSkip>, (const void *)kern<0, kSelList>,     \
+        (const void *)kern<1, kSelPlain>, (const void *)kern<1, kSelSkip>, (const void *)kern<1, kSelList>, \
+        (const void *)kern<2, kSelPlain>, (const void *)kern<2, kSelSkip>, (const void *)kern<2, kSelList>
+    for (const void *fn : {TSB_ALL_MODES(domino_multi_kernel), TSB_ALL_MODES(domino_multi1_kernel),
+                           TSB_ALL_MODES(domino_multi1c_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem)) != cudaSuccess)
             return bail(e, "smem attribute");
-    for (const void *fn : {(const void *)domino_multi_pipe_kernel<0>, (const void *)domino_multi_pipe_kernel<1>,
-                           (const void *)domino_multi_pipe_kernel<2>})
+    for (const void *fn : {TSB_ALL_MODES(domino_multi_pipe_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem)) != cudaSuccess)
             return bail(e, "smem attribute");
+#undef TSB_ALL_MODES
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
     if ((e = cudaMalloc(&h->tiles, sizeof(int2) * std::max<size_t>(1, tiles.size()))) != cudaSuccess)
         return bail(e, "cudaMalloc tiles");

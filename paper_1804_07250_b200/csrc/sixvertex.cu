@@ -522,12 +522,19 @@ void sv_multi_config(tsb_sv *h) {
         h->m_gx = (h->W + h->m_stride - 1) / h->m_stride;
     }
     int nw = 16, K = 8;
+    cudaDeviceGetAttribute(&h->m_sms, cudaDevAttrMultiProcessorCount, h->device);
+    // a single chain that fits one wave either way: 15 warps (14 exact rows per
+    // tile at K = 8) spread it over more SMs than 16 (DWBC 2048: 147 instead of
+    // 129 blocks; 1.83 -> 1.78 us per sweep at Delta = 1/2, 2.24 -> 2.16 at -3)
+    if (h->nchains == 1) {
+        const int b16 = h->m_gx * ((h->f + 15) / 16), b15 = h->m_gx * ((h->f + 13) / 14);
+        if (b15 <= h->m_sms && b15 > b16) nw = 15;
+    }
     if (const char *e = getenv("TSB_SV_NW")) nw = atoi(e) == 16 ? 16 : atoi(e) == 15 ? 15 : 8;
     if (const char *e = getenv("TSB_SV_K")) {
         K = atoi(e);
         h->m_k_fixed = true;
     }
-    cudaDeviceGetAttribute(&h->m_sms, cudaDevAttrMultiProcessorCount, h->device);
     if (K != 2 && K != 4 && K != 8 && K != 16) K = 4;
     while (2 * nw - 2 * K < 2) K /= 2;
     h->m_nw = nw;

@@ -49,9 +49,12 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     // loop below then runs two independent splitmix chains per lane without
     // a divergent tail (lanes of a warp issue together, so the padding costs
     // no issue slots)
-    const int padded = (total + 31) & ~31;
+#ifndef TSB_FIRE_PAD
+#define TSB_FIRE_PAD 1
+#endif
+    const int padded = TSB_FIRE_PAD ? (total + 31) & ~31 : total;
     __syncwarp();
-    if (lane < padded - total) queue[total + lane] = queue[0];
+    if (TSB_FIRE_PAD && lane < padded - total) queue[total + lane] = queue[0];
     __syncwarp();
     const uint64_t salt = (step + 1ull) * kGold;
     // site index i = r * side + column, column = 32 * (wa of lane 0) + col,
@@ -64,7 +67,7 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     };
     int j = lane;
     for (; j + 32 < padded; j += 64) {
-        const uint32_t q0 = queue[j], q1 = queue[j + 32];
+        const uint32_t q0 = queue[j], q1 = queue[j + 32];  // unpadded builds: j + 32 < total, both valid
         const uint32_t c0 = col_of(q0), c1 = col_of(q1);
         // two independent chains for ILP
         const uint64_t x0 = mix64_hot(mix64_hot(kb + (uint64_t)c0 * kGold) + salt);

@@ -287,6 +287,15 @@ class DominoHandle:
 
 _CACHE: "OrderedDict[tuple, DominoHandle]" = OrderedDict()
 _CACHE_MAX = 8
+_COLLAPSE: bool | None = None  # None: the library default (run collapsing on, env TSB_DOM_COLLAPSE)
+
+
+def set_default_collapse(on: bool | None) -> None:
+    """Run collapsing for the walks of the drop-in API (random_walk_batch,
+    random_walk, CFTP); None restores the library default.  Results are
+    bit-identical either way (tsb_domino_set_collapse)."""
+    global _COLLAPSE
+    _COLLAPSE = on
 
 
 def _handle_for(domain: Domain | None, nchains: int, side: int | None = None) -> DominoHandle:
@@ -300,6 +309,8 @@ def _handle_for(domain: Domain | None, nchains: int, side: int | None = None) ->
             _CACHE.popitem(last=False)
     else:
         _CACHE.move_to_end(key)
+    if _COLLAPSE is not None:
+        h.set_collapse(_COLLAPSE)
     return h
 
 
