@@ -238,8 +238,6 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
                                            uint16_t (*queue)[1024], int k, int lane, int z, int r, int wa,
                                            bool in_grid, uint4 cur, uint64_t step0) {
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
-    const uint32_t na0 = need_a(0, k, lane), na1 = need_a(1, k, lane), nb0 = need_b(0, k, lane),
-                   nb1 = need_b(1, k, lane);
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         uint64_t step;
@@ -260,12 +258,15 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vua & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act & (s ? na1 : na0);
+        uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act;
         const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
         const uint32_t ib = vub & cur.z & ~(lb | cur.w);
-        const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act & (s ? nb1 : nb0);
+        uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
+            // the masks only where coins are drawn: the frozen bulk never pays them
+            ra &= need_a(s, k, lane);
+            rb &= need_b(s, k, lane);
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
             f = warp_fire<TM>(ra, rb, ia, ib, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step);
         }
@@ -446,12 +447,12 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx 
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.y, 1);  // lane 0: halo, wraps harmlessly
         const uint32_t la = (cur.y << 1) | (hl >> 31);
         const uint32_t ia = vu & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act &
-                            (lane == 31 ? need_b(s, k, 31) : need_a(s, k, lane));
+        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act;
         uint32_t f = 0u;
         if (__any_sync(0xffffffffu, ra != 0u)) {
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
-            f = warp_fire<TM, 1>(ra, 0u, ia, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step).x;
+            const uint32_t rn = ra & (lane == 31 ? need_b(s, k, 31) : need_a(s, k, lane));
+            f = warp_fire<TM, 1>(rn, 0u, ia, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step).x;
         }
         fs[k][lane] = f;
         __syncthreads();
