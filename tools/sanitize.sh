@@ -23,12 +23,16 @@ for tool in memcheck synccheck racecheck; do
     run $tool TSB_DOM_PIPE=1 -- domino
     run $tool TSB_DOM_RESIDENT=1 -- domino
     run $tool TSB_DOM_RESIDENT=0 TSB_DOM_ADAPT=0 -- domino
+    run $tool TSB_DOM_COLLAPSE=0 -- domino
     run $tool -- cftp heights strips domain
+    run $tool TSB_DOM_RESIDENT=0 -- cftp
     run $tool -- sv
     run $tool TSB_SV_K=2 TSB_SV_NW=8 -- sv
     run $tool TSB_SV_WPL=1 -- sv
     run $tool TSB_SV_DENSE=1 -- sv
+    run $tool TSB_SV_COLLAPSE=0 -- sv
     run $tool -- loz
     run $tool TSB_LZ_K=2 -- loz
     run $tool TSB_LZ_DENSE=1 -- loz
+    run $tool TSB_LZ_COLLAPSE=0 -- loz
 done
