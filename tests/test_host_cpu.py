@@ -244,3 +244,36 @@ def test_c_abi_header_is_plain_c(tmp_path):
                     str(tmp_path / "t.o")], check=True)
     out = subprocess.run([str(tmp_path / "t")], capture_output=True, text=True, check=True).stdout
     assert out.strip() == "1"
+
+
+def test_bench_reference_arm_workload_is_package_free():
+    """bench.py's reference arm builds the Aztec workload in numpy (no
+    product import): its T_max, colour coins and per-colour vertex counts
+    equal the package's (closed form, rng.color_at, vertex_mask parity)."""
+    import subprocess
+    import sys
+
+    import numpy as np
+
+    import bench
+    from paper_1804_07250_b200 import rng
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+
+    for order in (1, 2, 3, 8, 63, 64, 257):
+        n = 2 * order
+        r = np.arange(n) + 0.5 - order
+        faces = (np.abs(r)[:, None] + np.abs(r)[None, :]) <= order
+        p = np.pad(faces, 1)
+        vm = p[:-1, :-1] | p[:-1, 1:] | p[1:, :-1] | p[1:, 1:]
+        rr = np.arange(n + 1)
+        even = ((rr[:, None] + rr[None, :]) & 1) == 0
+        assert bench.aztec_counts(order) == (int((vm & even).sum()), int((vm & ~even).sum()))
+        assert np.array_equal(bench.aztec_tmax_host(order), aztec_extremal_states(order)[0])
+    for s in (0x5EED, 1, 2**63 + 5):
+        assert [bench._color_at(s, k) for k in range(64)] == [rng.color_at(s, k) for k in range(64)]
+    # the reference arm's module-level imports do not pull in the product
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import bench; "
+            "print(any(m.startswith('paper_1804_07250_b200') for m in sys.modules))" % root)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "False"
