@@ -298,9 +298,9 @@ def set_default_collapse(on: bool | None) -> None:
     _COLLAPSE = on
 
 
-def _handle_for(domain: Domain | None, nchains: int, side: int | None = None) -> DominoHandle:
+def _handle_for(domain: Domain | None, nchains: int, side: int | None = None, slot: int = 0) -> DominoHandle:
     side = domain.n + 1 if domain is not None else side
-    key = (domain._key if domain is not None else None, side, nchains, _native.device())
+    key = (domain._key if domain is not None else None, side, nchains, _native.device(), slot)
     h = _CACHE.get(key)
     if h is None:
         h = DominoHandle(domain, side, nchains)
@@ -329,11 +329,44 @@ def random_walk_batch(
     seeds = np.asarray(seeds, dtype=np.uint64)
     if n_steps <= 0 or states.shape[0] == 0:
         return states.copy()  # a new array, like the reference (sweeps.py:299)
+    if states.shape[0] >= 2 and v * v >= _PIPELINE_MIN_BYTES:
+        return _walk_pipelined(states, seeds, n_steps, plan)
     h = _handle_for(plan.domain, states.shape[0]) if plan.domain.n + 1 == v else _handle_for(None, states.shape[0], v)
     h.set_plan(plan)
     h.upload(states)
     h.walk(seeds, n_steps)
     return h.download()
+
+
+_PIPELINE_MIN_BYTES = 1 << 22  # chains of at least 4 MB of tilestates: copies worth overlapping
+
+
+def _walk_pipelined(states: np.ndarray, seeds: np.ndarray, n_steps: int, plan: "SweepPlan") -> np.ndarray:
+    """random_walk_batch for large lattices: the chains alternate between two
+    one-chain handles, each on its own CUDA stream, so chain i+1's upload runs
+    while chain i walks and chain i's download while chain i+1 walks.  Every
+    chain's result depends on its own seed only (sweeps.py:286-292), so the
+    output equals the batched walk."""
+    v = states.shape[-1]
+    dom = plan.domain if plan.domain.n + 1 == v else None
+    hs = [_handle_for(dom, 1, v, slot=k) for k in (1, 2)]
+    for h in hs:
+        h.set_plan(plan)
+    out = np.empty_like(states)
+    pending = [None, None]
+    for i in range(states.shape[0]):
+        k = i & 1
+        if pending[k] is not None:
+            j = pending[k]
+            hs[k].download(out=out[j:j + 1])
+        hs[k].upload(states[i:i + 1])
+        hs[k].walk(seeds[i:i + 1], n_steps)
+        pending[k] = i
+    for k in (0, 1):
+        if pending[k] is not None:
+            j = pending[k]
+            hs[k].download(out=out[j:j + 1])
+    return out
 
 
 def sweep(

@@ -86,3 +86,19 @@ def test_lozenge_collapse_exact(abc, chains, steps):
         h.upload(start)
         h.walk(seeds, steps, step0=11)
         assert np.array_equal(h.download(), ref), on
+
+
+def test_random_walk_batch_pipelined():
+    """random_walk_batch on large lattices alternates the chains between two
+    one-chain handles on their own streams (copies of one chain overlap the
+    sweeps of the next): equal to the oracle for odd and even batch sizes."""
+    order = 1100  # 2201^2 = 4.8 MB of tilestates per chain: the pipelined path
+    d = ts.Domain.aztec(order)
+    plan = ts.SweepPlan(d)
+    t_max, t_min = aztec_extremal_states(order)
+    for b in (2, 3):
+        start = np.stack([t_max, t_min, t_max][:b])
+        seeds = np.arange(40, 40 + b, dtype=np.uint64)
+        out = ts.random_walk_batch(start, seeds, 37, plan)
+        assert np.array_equal(out, oracle.domino_walk(start, seeds, plan.p_up, 37)), b
+        assert out is not start and np.array_equal(start[0], t_max)  # a new array; input untouched
