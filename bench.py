@@ -261,6 +261,7 @@ def bench_config(args, world: int, strips: bool) -> dict:
             "domain_vertices": black + white, "sweeps_per_step": args.sweeps_per_step, "seed": SEED,
             "parallelism": (f"strips x{world}, halo {args.halo} rows exchanged every {args.halo} sweeps "
                             + ("(host NCCL p2p)" if args.host_exchange else "(device push/pull over peer memory)")
+                            + ", each rank holding only its window of rows"
                             if strips else (f"replicas x{world}" if world > 1 else "single chain")),
             "l2": "flushed (256 MiB write) between timed steps; state planes stay "
                   "L2-resident within a step by design"}
@@ -483,16 +484,24 @@ def main():
     strips = strips_mode(args, world)
     if strips:
         seed = SEED  # one chain sharded over all GPUs
-    h = DominoHandle(d, d.n + 1, 1)
-    h.set_collapse(False)  # the headline executes every sweep (run collapsing: the "collapsed" record)
-    h.set_stream(stream.cuda_stream)
-    h.set_plan(plan)
-    h.upload(t_max[None])
     if strips:
         from paper_1804_07250_b200.strips import (DeviceStripWalker, DominoStripEngine, StripWalker,
                                                   strip_bounds)
 
+        # memory-sharded: each rank holds only its strip plus halo rows
         bounds = strip_bounds(d.vertex_mask, world, min_rows=args.halo)
+        win = (max(0, bounds[rank] - args.halo), min(d.n + 1, bounds[rank + 1] + args.halo))
+        h = DominoHandle.window(d, win[0], win[1])
+    else:
+        h = DominoHandle(d, d.n + 1, 1)
+    h.set_collapse(False)  # the headline executes every sweep (run collapsing: the "collapsed" record)
+    h.set_stream(stream.cuda_stream)
+    h.set_plan(plan)
+    if strips:
+        h.upload_rows(win[0], t_max[win[0]:win[1]])
+    else:
+        h.upload(t_max[None])
+    if strips:
         row_engine = None
         if args.host_exchange:  # halo rows through torch.distributed (NCCL) from the host
             walker = StripWalker(None, bounds, rank, world, args.halo)
@@ -580,80 +589,45 @@ def main():
                       + " over DominoHandle; state resident, strip rows read back to pinned host each step",
                "clock": "host wall clock, max over ranks"}
     if not args.no_e2e and not strips:
-        # End to end through the public handle API with the reference's state
-        # layout: every step uploads the (B, V, V) uint8 tilestates from pinned
-        # host memory, walks S sweeps and downloads the new tilestates into
-        # pinned host memory; the output of step k is the input of step k+1.
+        # End to end through the drop-in API a reference user calls:
+        # random_walk_batch on a (2, V, V) uint8 numpy batch (pageable memory),
+        # every step uploading the tilestates, walking S sweeps and returning
+        # a new array that is the next step's input (sweeps.py:278-316).  Run
+        # collapsing off, like the headline.
+        from paper_1804_07250_b200 import sweeps as _sweeps
+
         side = d.n + 1
-        he = DominoHandle(d, side, 1)
-        he.set_collapse(False)
-        he.set_plan(plan)
-        bufs = [torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        bufs[0].numpy()[0] = t_max
-        he.upload(bufs[0].numpy())
-        he.walk([seed], S)  # warm the graph
-        he.download(out=bufs[1].numpy())
-        he.sync()
+        _sweeps.set_default_collapse(False)
+        states = np.stack([t_max, t_max])
+        ts.random_walk_batch(states, np.array([1, 2], dtype=np.uint64), S, plan)  # warm the handle and graph
         e2e_att = 0
         t0 = time.perf_counter()
         for k in range(args.steps):
-            sk = rng.derive_seed(seed, k, 7)
-            src, dst = bufs[k & 1].numpy(), bufs[(k + 1) & 1].numpy()
-            he.upload(src)              # H2D: tilestates (V*V B)
-            he.walk([sk], S)            # H2D: the seed (8 B); S sweeps
-            he.download(out=dst)        # D2H: tilestates (V*V B), synchronous
-            e2e_att += attempts_for(sk, 0, S, counts)
-        dt_serial = time.perf_counter() - t0
-        serial = e2e_att / dt_serial
-        # Streamed: two independent chains on two handles (two CUDA streams),
-        # each step still uploads its chain's tilestates from pinned memory,
-        # walks S sweeps and downloads the result, but chain A's transfers and
-        # host checks run while chain B walks, so the copies hide behind the
-        # sweeps.  Every upload, walk and download is inside the timed region.
-        hs = [he, DominoHandle(d, side, 1)]
-        hs[1].set_collapse(False)
-        hs[1].set_plan(plan)
-        sb = [bufs[0], torch.empty((1, side, side), dtype=torch.uint8, pin_memory=True)]
-        sb[1].numpy()[0] = t_max
-        hs[1].upload(sb[1].numpy())
-        hs[1].walk([seed ^ 1], S)  # warm the second graph
-        hs[1].download(out=sb[1].numpy())
-        for h in hs:
-            h.sync()
-        e2e_att = 0
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            h, b = hs[k & 1], sb[k & 1].numpy()
-            if k >= 2:
-                h.download(out=b)       # D2H: result of step k-2 (same chain)
-            sk = rng.derive_seed(seed, k, 11)
-            h.upload(b)                 # H2D: this step's tilestates
-            h.walk([sk], S)             # H2D seed; S sweeps, asynchronous
-            e2e_att += attempts_for(sk, 0, S, counts)
-        for k in range(max(0, args.steps - 2), args.steps):
-            hs[k & 1].download(out=sb[k & 1].numpy())
+            seeds_k = np.array([rng.derive_seed(seed, k, 7), rng.derive_seed(seed, k, 8)], dtype=np.uint64)
+            states = ts.random_walk_batch(states, seeds_k, S, plan)
+            e2e_att += sum(attempts_for(int(x), 0, S, counts) for x in seeds_k)
         dt = time.perf_counter() - t0
-        # the plain call a user makes with pageable numpy arrays, for reference
-        cur = ts.Tiling(d, bufs[0].numpy()[0].copy())
-        ts.random_walk(cur, seed, S, plan)
+        # the same with the library default (run collapsing on)
+        _sweeps.set_default_collapse(None)
+        ts.random_walk_batch(states, np.array([3, 4], dtype=np.uint64), S, plan)
+        att_c = 0
         t1 = time.perf_counter()
-        cur = ts.random_walk(cur, rng.derive_seed(seed, 99, 7), S, plan)
-        dt_plain = time.perf_counter() - t1
-        att_plain = attempts_for(rng.derive_seed(seed, 99, 7), 0, S, counts)
+        for k in range(args.steps):
+            seeds_k = np.array([rng.derive_seed(seed, k, 9), rng.derive_seed(seed, k, 10)], dtype=np.uint64)
+            states = ts.random_walk_batch(states, seeds_k, S, plan)
+            att_c += sum(attempts_for(int(x), 0, S, counts) for x in seeds_k)
+        dt_c = time.perf_counter() - t1
         e2e_v = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         e2e_a = torch.tensor([float(e2e_att)], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(e2e_v, op=dist.ReduceOp.MAX)
             dist.all_reduce(e2e_a, op=dist.ReduceOp.SUM)
         e2e = {"value": float(e2e_a.item()) / float(e2e_v.item()), "unit": UNIT,
-               "h2d_bytes_per_step": side * side + 8, "d2h_bytes_per_step": side * side,
-               "api": "DominoHandle.upload / walk / download (reference uint8 tilestates, pinned host buffers), "
-                      "two chains on two handles streamed so one chain's copies overlap the other's sweeps; "
-                      "host wall clock",
-               "serial_one_chain": serial * world,
-               "random_walk_pageable": att_plain / dt_plain,
-               "random_walk_pageable_note": "ts.random_walk on pageable numpy arrays, library defaults "
-                                            "(run collapsing on)"}
+               "h2d_bytes_per_step": 2 * side * side + 16, "d2h_bytes_per_step": 2 * side * side,
+               "api": "paper_1804_07250_b200.random_walk_batch on a (2, V, V) uint8 numpy batch in pageable "
+                      "memory (the reference's call, sweeps.py:278-316): upload, S sweeps per chain, new array "
+                      "back, every step; run collapsing off; host wall clock",
+               "collapsed_library_default": att_c / dt_c}
 
     warm = collapsed = None
     if not args.no_warm and not strips and args.order == 4096:

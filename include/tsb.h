@@ -76,6 +76,20 @@ typedef struct tsb_domino tsb_domino;
  * it bounds the work region and the crossable edges. */
 int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, tsb_domino **out);
 int tsb_domino_destroy(tsb_domino *h);
+/* One chain of the `side` x `side` grid holding only the global rows
+ * [row_lo, row_hi) (plus a zero margin): state planes, domain planes and
+ * tiles cover the window, so N strip ranks hold 1/N of a lattice each.
+ * Rows keep their global indices (coins and colours are unchanged).  Whole-grid
+ * operations (upload / download / heights / extremal / cftp / observables)
+ * fail with TSB_E_VALUE; use tsb_domino_upload_rows / download_rows.  `faces`
+ * is the full (side-1)^2 grid (NULL: all faces). */
+int tsb_domino_create_window(int device, int side, int row_lo, int row_hi, const uint8_t *faces, tsb_domino **out);
+/* Rows [r0, r0+nrows) of chain 0 from / to a host (nrows, side) uint8
+ * tilestate grid (the reference layout); any handle, rows within its window.
+ * The "up" bit of a window's first row refers to a row the window does not
+ * hold: it is not checked on upload and reads back as 0. */
+int tsb_domino_upload_rows(tsb_domino *h, int r0, int nrows, const uint8_t *rows);
+int tsb_domino_download_rows(tsb_domino *h, int r0, int nrows, uint8_t *rows);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
 int tsb_domino_set_stream(tsb_domino *h, void *stream);
 /* SweepPlan.p_up, (side x side) float64 (sweeps.py:170-179).  Converted

@@ -83,6 +83,9 @@ _SIGS = {
     "tsb_uniform_grid": (_i, [_i, _u64, _i, _i, _u64, _i, _vp]),
     "tsb_domino_create": (_i, [_i, _i, _i, _vp, _vp]),
     "tsb_domino_destroy": (_i, [_vp]),
+    "tsb_domino_create_window": (_i, [_i, _i, _i, _i, _vp, _vp]),
+    "tsb_domino_upload_rows": (_i, [_vp, _i, _i, _vp]),
+    "tsb_domino_download_rows": (_i, [_vp, _i, _i, _vp]),
     "tsb_domino_set_stream": (_i, [_vp, _vp]),
     "tsb_domino_set_p_up": (_i, [_vp, _vp]),
     "tsb_domino_set_p_up_parity": (_i, [_vp, ctypes.c_double, ctypes.c_double]),

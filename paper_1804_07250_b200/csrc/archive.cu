@@ -77,6 +77,7 @@ using namespace tsb;
 extern "C" {
 
 int tsb_domino_serialize(tsb_domino *h, int chain, char *out, size_t cap, size_t *len) {
+    TSB_FULL_ONLY(h);
     if (!h || !len) return fail(TSB_E_VALUE, "null argument");
     if (chain < 0 || chain >= h->nchains) return fail(TSB_E_VALUE, "chain %d out of range", chain);
     TSB_CUDA(cudaSetDevice(h->device));

@@ -52,6 +52,7 @@ using namespace tsb;
 extern "C" {
 
 int tsb_domino_coalesced(tsb_domino *h, int chain0, int npairs, uint8_t *flags) {
+    TSB_FULL_ONLY(h);
     int rc = check_range(h, chain0, 2 * npairs);
     if (rc || npairs == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
@@ -68,6 +69,7 @@ int tsb_domino_coalesced(tsb_domino *h, int chain0, int npairs, uint8_t *flags) 
 }
 
 int tsb_domino_replicate(tsb_domino *h, int src, int dst0, int step, int n) {
+    TSB_FULL_ONLY(h);
     if (!h) return fail(TSB_E_VALUE, "null handle");
     if (n <= 0) return TSB_OK;
     if (src < 0 || src >= h->nchains || dst0 < 0 || step < 1 || dst0 + (int64_t)(n - 1) * step >= h->nchains)
@@ -84,6 +86,7 @@ int tsb_domino_cftp(tsb_domino *h, const uint8_t *top0, const uint8_t *bot0, con
                     int count, int max_doublings, uint8_t *out_states, int32_t *collapsed_round,
                     tsb_progress_fn progress, void *user) {
     if (!h || !top0 || !bot0 || !masters || !out_states) return fail(TSB_E_VALUE, "null argument");
+    TSB_FULL_ONLY(h);
     if (count <= 0) return TSB_OK;
     if (h->nchains < 2 * count + 2)
         return fail(TSB_E_VALUE, "handle needs >= %d chains for %d samples", 2 * count + 2, count);

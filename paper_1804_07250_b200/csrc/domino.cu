@@ -698,9 +698,9 @@ __device__ __forceinline__ bool face_in(const uint8_t *faces, int nf, int r, int
 }
 
 __global__ void domain_planes_kernel(const uint8_t *faces, int side, int W, int pitch,
-                                     uint4 *dom, uint32_t *fbits, int2 *range) {
+                                     uint4 *dom, uint32_t *fbits, int2 *range, int r0, int win_lo, int win_hi) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = blockIdx.y;
+    const int r = r0 + (int)blockIdx.y;  // global row (row windows: only the allocated rows)
     if (w >= W) return;
     const int nf = side - 1;
     uint32_t cv = 0, ch = 0, ev = 0, eh = 0, fb = 0;
@@ -719,7 +719,7 @@ __global__ void domain_planes_kernel(const uint8_t *faces, int side, int W, int 
     }
     dom[(size_t)r * pitch + w] = make_uint4(cv, ch, ev, eh);
     fbits[(size_t)r * pitch + w] = fb;
-    if (any) {
+    if (any && r >= win_lo && r < win_hi) {  // swept rows: the window's (tiles never start outside it)
         atomicMin(&range[r].x, w);
         atomicMax(&range[r].y, w + 1);
     }
@@ -774,6 +774,50 @@ __global__ void unpack_kernel(const uint2 *state, int side, int pitch, size_t ch
     const uint32_t rt = (s[w].y >> b) & 1u;
     const uint32_t lf = cc > 0 ? (s[(cc - 1) >> 5].y >> ((cc - 1) & 31)) & 1u : 0u;
     bytes[(size_t)z * side * side + (size_t)r * side + cc] = (uint8_t)(up | dn << 1 | lf << 2 | rt << 3);
+}
+
+// Rows [r0, r0 + gridDim.y) of chain 0 from / to a (rows, side) uint8 grid
+// (row windows, host-driven strip exchange): the same codec as pack_kernel /
+// unpack_kernel; the first row's "up" bits are not checked (the row above is
+// not in the grid).
+__global__ void pack_rows_kernel(const uint8_t *bytes, int r0, int side, int W, int pitch, const uint4 *dom,
+                                 uint2 *state, int *bad) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, r = r0 + i;
+    if (w >= W) return;
+    const uint8_t *g = bytes + (size_t)i * side;
+    const uint4 cr = dom[(size_t)r * pitch + w];
+    uint32_t v = 0, hz = 0;
+    int err = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int cc = w * 32 + b;
+        if (cc >= side) break;
+        const uint8_t st = g[cc];
+        if (st >= 16) err |= 1;
+        const bool up = st & 1, dn = st & 2, lf = st & 4, rt = st & 8;
+        const bool lf_n = cc > 0 ? (g[cc - 1] & 8) != 0 : false;
+        if (lf != lf_n) err |= 2;
+        if (i > 0 && up != ((g[cc - side] & 2) != 0)) err |= 2;
+        if (dn && !((cr.x >> b) & 1u)) err |= 4;
+        if (rt && !((cr.y >> b) & 1u)) err |= 4;
+        if (dn) v |= 1u << b;
+        if (rt) hz |= 1u << b;
+    }
+    state[(size_t)(r + 1) * pitch + w] = make_uint2(v, hz);
+    if (err) atomicOr(bad, err);
+}
+
+__global__ void unpack_rows_kernel(const uint2 *state, int r0, int side, int pitch, uint8_t *bytes) {
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, r = r0 + i;
+    if (cc >= side) return;
+    const uint2 *s = state + (size_t)(r + 1) * pitch;
+    const int w = cc >> 5, b = cc & 31;
+    const uint32_t up = (s[w - pitch].x >> b) & 1u;
+    const uint32_t dn = (s[w].x >> b) & 1u;
+    const uint32_t rt = (s[w].y >> b) & 1u;
+    const uint32_t lf = cc > 0 ? (s[(cc - 1) >> 5].y >> ((cc - 1) & 31)) & 1u : 0u;
+    bytes[(size_t)i * side + cc] = (uint8_t)(up | dn << 1 | lf << 2 | rt << 3);
 }
 
 }  // namespace tsb
@@ -1103,7 +1147,7 @@ int ensure_graph(tsb_domino *h, int chain0, int n, bool compact) {
 int settle(tsb_domino *h, int chain0, int n, int cur0) {
     if (h->cur == cur0 || n == h->nchains) return TSB_OK;
     const size_t off = (size_t)chain0 * h->chain_stride;
-    TSB_CUDA(cudaMemcpyAsync(h->buf[h->cur ^ 1] + off, h->buf[h->cur] + off,
+    TSB_CUDA(cudaMemcpyAsync(h->buf_alloc[h->cur ^ 1] + off, h->buf_alloc[h->cur] + off,
                              sizeof(uint2) * h->chain_stride * n, cudaMemcpyDeviceToDevice, h->stream));
     h->cur ^= 1;
     return TSB_OK;
@@ -1113,7 +1157,25 @@ int settle(tsb_domino *h, int chain0, int n, int cur0) {
 
 extern "C" {
 
+static int create_impl(int device, int side, int nchains, const uint8_t *faces, int row_lo, int row_hi,
+                       tsb_domino **out);
+
 int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, tsb_domino **out) {
+    return create_impl(device, side, nchains, faces, 0, side, out);
+}
+
+int tsb_domino_create_window(int device, int side, int row_lo, int row_hi, const uint8_t *faces, tsb_domino **out) {
+    if (row_lo < 0 || row_hi > side || row_hi <= row_lo) return fail(TSB_E_VALUE, "window rows out of range");
+    return create_impl(device, side, 1, faces, row_lo, row_hi, out);
+}
+
+// Rows beyond a window that its tiles may load or store: a multi-sweep tile
+// reaches kMK + kMOut - 1 rows past the window edge, a single-sweep tile
+// kTileRows (zero there: the stale halo a strip never reads back).
+constexpr int kWinMargin = 16;
+
+static int create_impl(int device, int side, int nchains, const uint8_t *faces, int row_lo, int row_hi,
+                       tsb_domino **out) {
     if (!out) return fail(TSB_E_VALUE, "null output pointer");
     *out = nullptr;
     if (side < 1 || nchains < 1) return fail(TSB_E_VALUE, "side and nchains must be positive");
@@ -1133,7 +1195,11 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     // load and store inside the row
     const int nchunks_ = (h->W + 1 + kTileWords - 1) / kTileWords;
     h->pitch = (std::max(kPad + nchunks_ * kTileWords + 2, kPad + h->W + 64) + 31) / 32 * 32;
-    h->chain_stride = (size_t)(side + 2) * h->pitch;
+    h->windowed = row_lo > 0 || row_hi < side;
+    h->row_a = h->windowed ? std::max(-1, row_lo - kWinMargin) : -1;
+    h->row_b = h->windowed ? std::min(side + 1, row_hi + kWinMargin) : side + 1;
+    h->chain_stride = (size_t)(h->row_b - h->row_a) * h->pitch;
+    const int da = std::max(0, h->row_a), db = std::min(side, h->row_b);  // allocated rows of the domain planes
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaStreamCreate"); }
     h->own_stream = true;
@@ -1144,13 +1210,16 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     };
     const size_t sbytes = sizeof(uint2) * h->chain_stride * nchains;
     for (int i = 0; i < 2; ++i) {
-        if ((e = cudaMalloc(&h->buf[i], sbytes)) != cudaSuccess) return bail(e, "cudaMalloc state");
-        if ((e = cudaMemsetAsync(h->buf[i], 0, sbytes, h->stream)) != cudaSuccess) return bail(e, "memset");
+        if ((e = cudaMalloc(&h->buf_alloc[i], sbytes)) != cudaSuccess) return bail(e, "cudaMalloc state");
+        if ((e = cudaMemsetAsync(h->buf_alloc[i], 0, sbytes, h->stream)) != cudaSuccess) return bail(e, "memset");
+        h->buf[i] = h->buf_alloc[i] - (ptrdiff_t)(h->row_a + 1) * h->pitch;  // global row indexing
     }
-    if ((e = cudaMalloc(&h->dom, sizeof(uint4) * (size_t)side * h->pitch)) != cudaSuccess)
+    if ((e = cudaMalloc(&h->dom_alloc, sizeof(uint4) * (size_t)(db - da) * h->pitch)) != cudaSuccess)
         return bail(e, "cudaMalloc dom");
-    if ((e = cudaMalloc(&h->fbits, sizeof(uint32_t) * (size_t)side * h->pitch)) != cudaSuccess)
+    if ((e = cudaMalloc(&h->fbits_alloc, sizeof(uint32_t) * (size_t)(db - da) * h->pitch)) != cudaSuccess)
         return bail(e, "cudaMalloc fbits");
+    h->dom = h->dom_alloc - (ptrdiff_t)da * h->pitch;
+    h->fbits = h->fbits_alloc - (ptrdiff_t)da * h->pitch;
     if ((e = cudaMalloc(&h->range, sizeof(int2) * side)) != cudaSuccess) return bail(e, "cudaMalloc range");
     if ((e = cudaMalloc(&h->seedinfo, sizeof(uint64_t) * 2 * nchains)) != cudaSuccess)
         return bail(e, "cudaMalloc seeds");
@@ -1173,8 +1242,9 @@ int tsb_domino_create(int device, int side, int nchains, const uint8_t *faces, t
     if (e != cudaSuccess) { cudaFree(dfaces); return bail(e, "faces upload"); }
     std::vector<int2> init(side, make_int2(INT_MAX, INT_MIN));
     cudaMemcpyAsync(h->range, init.data(), sizeof(int2) * side, cudaMemcpyHostToDevice, h->stream);
-    domain_planes_kernel<<<dim3((h->W + 127) / 128, side), 128, 0, h->stream>>>(dfaces, side, h->W,
-                                                                               h->pitch, h->dom, h->fbits, h->range);
+    domain_planes_kernel<<<dim3((h->W + 127) / 128, db - da), 128, 0, h->stream>>>(
+        dfaces, side, h->W, h->pitch, h->dom, h->fbits, h->range, da, h->windowed ? row_lo : 0,
+        h->windowed ? row_hi : side);
     fix_ranges_kernel<<<(side + 255) / 256, 256, 0, h->stream>>>(h->range, side);
     e = cudaStreamSynchronize(h->stream);
     cudaFree(dfaces);
@@ -1295,10 +1365,10 @@ int tsb_domino_destroy(tsb_domino *h) {
     cudaSetDevice(h->device);
     strip_free(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    cudaFree(h->buf[0]);
-    cudaFree(h->buf[1]);
-    cudaFree(h->dom);
-    cudaFree(h->fbits);
+    cudaFree(h->buf_alloc[0]);
+    cudaFree(h->buf_alloc[1]);
+    cudaFree(h->dom_alloc);
+    cudaFree(h->fbits_alloc);
     cudaFree(h->range);
     cudaFree(h->xlist);
     cudaFree(h->xcnt);
@@ -1374,6 +1444,7 @@ int tsb_domino_set_p_up_parity(tsb_domino *h, double p_even, double p_odd) {
 }
 
 int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states) {
+    TSB_FULL_ONLY(h);
     int rc = check_range(h, chain0, n);
     if (rc || n == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
@@ -1395,6 +1466,7 @@ int tsb_domino_upload(tsb_domino *h, int chain0, int n, const uint8_t *states) {
 }
 
 int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states) {
+    TSB_FULL_ONLY(h);
     int rc = check_range(h, chain0, n);
     if (rc || n == 0) return rc;
     TSB_CUDA(cudaSetDevice(h->device));
@@ -1404,6 +1476,48 @@ int tsb_domino_download(tsb_domino *h, int chain0, int n, uint8_t *states) {
         h->buf[h->cur] + (size_t)chain0 * h->chain_stride + kPad, h->side, h->pitch, h->chain_stride, h->bytes);
     TSB_CUDA(cudaGetLastError());
     return staged_d2h(states, h->bytes, grid * n, h->stream);
+}
+
+static int rows_range(tsb_domino *h, int r0, int nrows) {
+    if (!h) return fail(TSB_E_VALUE, "null handle");
+    const int lo = std::max(0, h->row_a), hi = std::min(h->side, h->row_b);
+    if (nrows < 0 || r0 < lo || r0 + nrows > hi)
+        return fail(TSB_E_VALUE, "rows [%d, %d) outside the handle's rows [%d, %d)", r0, r0 + nrows, lo, hi);
+    return TSB_OK;
+}
+
+int tsb_domino_upload_rows(tsb_domino *h, int r0, int nrows, const uint8_t *rows) {
+    int rc = rows_range(h, r0, nrows);
+    if (rc || nrows == 0) return rc;
+    if (!rows) return fail(TSB_E_VALUE, "null rows");
+    TSB_CUDA(cudaSetDevice(h->device));
+    const size_t bytes = (size_t)nrows * h->side;
+    if ((rc = ensure_bytes(h, bytes))) return rc;
+    if ((rc = staged_h2d(h->bytes, rows, bytes, h->stream))) return rc;
+    TSB_CUDA(cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
+    pack_rows_kernel<<<dim3((h->W + 127) / 128, nrows), 128, 0, h->stream>>>(h->bytes, r0, h->side, h->W, h->pitch,
+                                                                              h->dom, h->buf[h->cur] + kPad, h->bad);
+    TSB_CUDA(cudaGetLastError());
+    int bad = 0;
+    TSB_CUDA(cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    TSB_CUDA(cudaStreamSynchronize(h->stream));
+    if (bad & 1) return fail(TSB_E_INCONSISTENT, "tilestate values must be < 16");
+    if (bad & 2) return fail(TSB_E_INCONSISTENT, "edge bit not mirrored by the neighbouring vertex");
+    if (bad & 4) return fail(TSB_E_INCONSISTENT, "crossed edge leaves the grid or the domain");
+    return TSB_OK;
+}
+
+int tsb_domino_download_rows(tsb_domino *h, int r0, int nrows, uint8_t *rows) {
+    int rc = rows_range(h, r0, nrows);
+    if (rc || nrows == 0) return rc;
+    if (!rows) return fail(TSB_E_VALUE, "null rows");
+    TSB_CUDA(cudaSetDevice(h->device));
+    const size_t bytes = (size_t)nrows * h->side;
+    if ((rc = ensure_bytes(h, bytes))) return rc;
+    unpack_rows_kernel<<<dim3((h->side + 127) / 128, nrows), 128, 0, h->stream>>>(h->buf[h->cur] + kPad, r0, h->side,
+                                                                                   h->pitch, h->bytes);
+    TSB_CUDA(cudaGetLastError());
+    return staged_d2h(rows, h->bytes, bytes, h->stream);
 }
 
 int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uint64_t step0,
@@ -1432,7 +1546,7 @@ int tsb_domino_walk(tsb_domino *h, int chain0, int n, const uint64_t *seeds, uin
 static size_t resident_smem(const tsb_domino *h, int n) {
     const char *ev = getenv("TSB_DOM_RESIDENT");  // 0: never, 1: whenever it fits (read per walk)
     const int mode = ev ? atoi(ev) : -1;
-    if (mode == 0 || h->strip || h->win_mn != h->nmtiles || h->win_tn != h->ntiles) return 0;
+    if (mode == 0 || h->strip || h->windowed || h->win_mn != h->nmtiles || h->win_tn != h->ntiles) return 0;
     const size_t items = (size_t)h->side * h->W;
     if (mode < 0 && items > (size_t)kResMaxItems && n < kResMinChains) return 0;
     const size_t bytes = kResScratch + sizeof(uint2) * (size_t)(h->side + 2) * h->W +

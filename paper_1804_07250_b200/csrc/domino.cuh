@@ -8,7 +8,15 @@
 struct tsb_domino {
     int device = 0, side = 0, nchains = 0, W = 0, pitch = 0;
     size_t chain_stride = 0;  // uint2 elements per chain
-    uint2 *buf[2] = {nullptr, nullptr};
+    uint2 *buf[2] = {nullptr, nullptr};  // row r of chain c at buf + c * chain_stride + (r + 1) * pitch (global r)
+    uint2 *buf_alloc[2] = {nullptr, nullptr};  // allocations (== buf unless windowed)
+    // row windows (tsb_domino_create_window): only global rows [row_a, row_b)
+    // are allocated (state, domain planes); buf / dom / fbits are offset so
+    // that kernels index global rows
+    bool windowed = false;
+    int row_a = -1, row_b = 0;
+    uint4 *dom_alloc = nullptr;
+    uint32_t *fbits_alloc = nullptr;
     int cur = 0;
     uint4 *dom = nullptr;        // {crossable V, crossable H, existing V, existing H} per word
     uint32_t *fbits = nullptr;   // face (r, c) in the domain
@@ -77,6 +85,13 @@ struct tsb_domino {
 constexpr int kGraphSweeps = 64;
 constexpr int kStatePad = 2;  // == kPad in domino.cu: zero words left of every state row
 
+
+// whole-grid operations are not available on row-window handles
+#define TSB_FULL_ONLY(h)                                                                       \
+    do {                                                                                       \
+        if ((h) && (h)->windowed)                                                              \
+            return tsb::fail(TSB_E_VALUE, "whole-grid operation on a row-window handle");      \
+    } while (0)
 
 namespace tsb {
 int ensure_bytes(tsb_domino *h, size_t need);

@@ -476,6 +476,7 @@ using namespace tsb;
 extern "C" {
 
 int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *out) {
+    TSB_FULL_ONLY(h);
     if (!h || !out) return fail(TSB_E_VALUE, "null argument");
     if (chain < 0 || chain >= h->nchains) return fail(TSB_E_VALUE, "chain %d out of range", chain);
     if (ref_r < 0 || ref_c < 0 || ref_r >= h->side || ref_c >= h->side)
@@ -492,6 +493,7 @@ int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *
 }
 
 int tsb_domino_height_sum_add(tsb_domino *h, int chain0, int n, int ref_r, int ref_c, long long *acc_dev) {
+    TSB_FULL_ONLY(h);
     int rc = check_range(h, chain0, n);
     if (rc || n == 0) return rc;
     if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");
@@ -506,6 +508,7 @@ int tsb_domino_height_sum_add(tsb_domino *h, int chain0, int n, int ref_r, int r
 // Returns TSB_E_UNTILEABLE (no exception message needed) when the domain has
 // no tiling, mirroring extremal_tilings() -> None.
 int tsb_domino_extremal(tsb_domino *h, int chain_max, int chain_min, int ref_r, int ref_c) {
+    TSB_FULL_ONLY(h);
     if (!h) return fail(TSB_E_VALUE, "null handle");
     if (chain_max < 0 || chain_max >= h->nchains || chain_min < 0 || chain_min >= h->nchains)
         return fail(TSB_E_VALUE, "chain out of range");

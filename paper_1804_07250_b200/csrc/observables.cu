@@ -44,6 +44,7 @@ using namespace tsb;
 extern "C" {
 
 int tsb_domino_orientation_add(tsb_domino *h, int chain0, int n, uint32_t *acc_dev) {
+    TSB_FULL_ONLY(h);
     int rc = check_range(h, chain0, n);
     if (rc || n == 0) return rc;
     if (!acc_dev) return fail(TSB_E_VALUE, "null accumulator");

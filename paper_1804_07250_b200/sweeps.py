@@ -206,6 +206,41 @@ class DominoHandle:
                                           None if faces is None else _native.ptr(faces),
                                           ctypes.byref(self._h)))
 
+    @classmethod
+    def window(cls, domain: Domain, row_lo: int, row_hi: int, device: int | None = None) -> "DominoHandle":
+        """One chain holding only the global rows [row_lo, row_hi) of the
+        domain's grid (tsb_domino_create_window): a strip rank's share of a
+        lattice.  Rows keep their global indices; use upload_rows /
+        download_rows (whole-grid operations raise ValueError)."""
+        h = cls.__new__(cls)
+        L = _native.lib()
+        h.side = domain.n + 1
+        h.nchains = 1
+        h.device = _native.device() if device is None else device
+        h.domain = domain
+        h._p_up_id = None
+        h._p_up_ref = None
+        h._h = ctypes.c_void_p()
+        h.rows = (row_lo, row_hi)
+        _native.check(L.tsb_domino_create_window(h.device, h.side, row_lo, row_hi, _native.ptr(domain.faces_u8),
+                                                 ctypes.byref(h._h)))
+        return h
+
+    def upload_rows(self, r0: int, rows: np.ndarray):
+        """Rows [r0, r0 + len(rows)) of chain 0 from a (n, V) uint8 tilestate grid."""
+        g = np.ascontiguousarray(rows, dtype=np.uint8)
+        if g.ndim != 2 or g.shape[1] != self.side:
+            raise ValueError(f"rows must have shape (n, {self.side})")
+        _native.check(_native.lib().tsb_domino_upload_rows(self._h, int(r0), g.shape[0], _native.ptr(g)))
+
+    def download_rows(self, r0: int, nrows: int, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((nrows, self.side), dtype=np.uint8)
+        elif out.shape != (nrows, self.side) or out.dtype != np.uint8 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous uint8 array of shape {(nrows, self.side)}")
+        _native.check(_native.lib().tsb_domino_download_rows(self._h, int(r0), int(nrows), _native.ptr(out)))
+        return out
+
     def __del__(self):
         try:
             if self._h:

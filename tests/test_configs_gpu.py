@@ -151,6 +151,34 @@ def test_c4_aztec_16384_strips(c4, world, halo):
     assert fp(got) == g["walk_100"]
 
 
+@pytest.mark.parametrize("world,halo", [(2, 64), (8, 64)])
+def test_c4_aztec_16384_memory_sharded_strips(c4, world, halo):
+    """C4 with memory-sharded strips: each window handle holds only its strip
+    plus halo (tsb_domino_create_window), uploaded and read back by rows."""
+    from paper_1804_07250_b200.strips import DeviceStripWalker, strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    g, d, t_max = c4
+    plan = ts.SweepPlan(d)
+    bounds = strip_bounds(d.vertex_mask, world, min_rows=halo)
+    hs = []
+    for r in range(world):
+        a, b = max(0, bounds[r] - halo), min(d.n + 1, bounds[r + 1] + halo)
+        h = DominoHandle.window(d, a, b, device=0)
+        h.set_plan(plan)
+        h.upload_rows(a, t_max[a:b])
+        hs.append(h)
+    ws = DeviceStripWalker.local(hs, bounds, halo)
+    DeviceStripWalker.walk_lockstep(ws, SEED, 100)
+    got = np.empty_like(t_max)
+    for w in ws:
+        got[w.lo:w.hi] = w.handle.download_rows(w.lo, w.hi - w.lo)
+        w.close()
+    del hs, ws
+    assert _bands(got) == g["bands_100"]
+    assert fp(got) == g["walk_100"]
+
+
 # ------------------------------------------------------------------- C5
 def test_c5_cftp_aztec_512_early_rounds():
     """The device CFTP driver's top/bottom chains after rounds 1..13 equal the

@@ -185,3 +185,74 @@ def test_lozenge_and_sixvertex_cftp_spread_over_processes(tmp_path):
     assert np.array_equal(np.load(tmp_path / "loz.npy"), np.stack([t.edges for t in loz]))
     assert np.array_equal(np.load(tmp_path / "sv.npy"),
                           np.stack([np.concatenate([c.h_edges.ravel(), c.v_edges.ravel()]) for c in sv]))
+
+
+def _window_walkers(d, plan, t_max, world, halo):
+    from paper_1804_07250_b200.strips import DeviceStripWalker, strip_bounds
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    bounds = strip_bounds(d.vertex_mask, world, min_rows=halo)
+    hs = []
+    for r in range(world):
+        a, b = max(0, bounds[r] - halo), min(d.n + 1, bounds[r + 1] + halo)
+        h = DominoHandle.window(d, a, b, device=0)
+        h.set_plan(plan)
+        h.upload_rows(a, t_max[a:b])
+        hs.append(h)
+    return hs, DeviceStripWalker.local(hs, bounds, halo)
+
+
+@pytest.mark.parametrize("world,halo,steps", [(2, 32, 300), (3, 24, 250), (4, 16, 97)])
+def test_device_strips_row_windows(world, halo, steps):
+    """Memory-sharded strips: every rank's handle holds only its window
+    (tsb_domino_create_window); the concatenated strips equal one walk."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+
+    order = 300
+    d = ts.Domain.aztec(order)
+    plan = ts.SweepPlan(d)
+    t_max, _ = aztec_extremal_states(order)
+    hs, ws = _window_walkers(d, plan, t_max, world, halo)
+    from paper_1804_07250_b200.strips import DeviceStripWalker
+
+    DeviceStripWalker.walk_lockstep(ws, SEED, steps, step0=5)
+    got = np.concatenate([w.handle.download_rows(w.lo, w.hi - w.lo) for w in ws])
+    for w in ws:
+        w.close()
+    assert np.array_equal(got, oracle_walk(t_max, plan.p_up, steps, 5))
+
+
+def test_row_window_handle_api():
+    """Row windows: whole-grid operations raise, rows round-trip, and a
+    window walked alone equals the full walk on rows far from its edges."""
+    import paper_1804_07250_b200 as ts
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+    from paper_1804_07250_b200.sweeps import DominoHandle
+
+    order = 200
+    d = ts.Domain.aztec(order)
+    plan = ts.SweepPlan(d)
+    t_max, _ = aztec_extremal_states(order)
+    a, b = 100, 260
+    h = DominoHandle.window(d, a, b, device=0)
+    h.set_plan(plan)
+    h.upload_rows(a, t_max[a:b])
+    # the window's first row has no row above it: its "up" bits read back as 0
+    assert np.array_equal(h.download_rows(a + 1, b - a - 1), t_max[a + 1:b])
+    with pytest.raises(ValueError):
+        h.download()
+    with pytest.raises(ValueError):
+        h.upload(t_max[None])
+    with pytest.raises(ValueError):
+        h.heights(0, d.reference_vertex)
+    with pytest.raises(ValueError):
+        h.upload_rows(a - 40, t_max[a - 40:a])  # outside the window
+    steps = 20
+    h.walk([SEED], steps)
+    ref = oracle_walk(t_max, plan.p_up, steps, 0)
+    # rows at least `steps` away from the window edges are exact
+    assert np.array_equal(h.download_rows(a + steps, b - a - 2 * steps), ref[a + steps:b - steps])
+    full = DominoHandle(d, d.n + 1, 1, device=0)
+    full.upload(t_max[None])
+    assert np.array_equal(full.download_rows(7, 50), t_max[7:57])
