@@ -79,6 +79,43 @@ struct SweepCtx {
 // strip walks); 2 compacted executed-sweep lists (run-collapsed walks).
 enum { kSelPlain = 0, kSelSkip = 1, kSelList = 2 };
 
+// Both sweeps of a kMK = 2 launch resolved up front, so their loads (list
+// cursor, entries / colour bytes) are in flight together instead of one
+// dependent round trip per sweep.
+struct Sweeps2 {
+    uint64_t step0, step1;
+    int color0, color1;
+    bool on0, on1;
+};
+
+template <int MODE>
+__device__ __forceinline__ Sweeps2 sweeps_of(const SweepCtx &c, int z, uint64_t step0) {
+    Sweeps2 w;
+    if constexpr (MODE == kSelList) {
+        const uint64_t j = *c.xbase + c.step;
+        const int n = c.xcnt[z];
+        const uint32_t *l = c.xlist + (size_t)z * c.xpitch;
+        const uint64_t base = c.step_dev[0];
+        w.on0 = j < (uint64_t)n;
+        w.on1 = j + 1 < (uint64_t)n;
+        const uint32_t e0 = w.on0 ? l[j] : 0u, e1 = w.on1 ? l[j + 1] : 0u;
+        w.step0 = base + (e0 & 0x7FFFFFFFu);
+        w.step1 = base + (e1 & 0x7FFFFFFFu);
+        w.color0 = (int)(e0 >> 31);
+        w.color1 = (int)(e1 >> 31);
+    } else {
+        const uint8_t *cl = c.colors + z * kGraphSweeps + (int)c.step;
+        const int c0 = cl[0], c1 = cl[1];
+        w.step0 = step0;
+        w.step1 = step0 + 1ull;
+        w.color0 = c0 & 1;
+        w.color1 = c1 & 1;
+        w.on0 = MODE == kSelPlain || !(c0 & 2);
+        w.on1 = MODE == kSelPlain || !(c1 & 2);
+    }
+    return w;
+}
+
 // Step and colour of sweep s of a multi-sweep launch for chain z; false when
 // the sweep is not executed (a collapsed run, or past the chain's list).
 template <int MODE>
@@ -238,11 +275,13 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
                                            uint16_t (*queue)[1024], int k, int lane, int z, int r, int wa,
                                            bool in_grid, uint4 cur, uint64_t step0) {
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
+    static_assert(kMK == 2, "two sweeps per launch");
+    const Sweeps2 sw = sweeps_of<MODE>(c, z, step0);
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
-        uint64_t step;
-        int color;
-        if (!sweep_of<MODE>(c, z, s, step0, &step, &color)) continue;  // block-uniform
+        if (!(s ? sw.on1 : sw.on0)) continue;  // block-uniform
+        const uint64_t step = s ? sw.step1 : sw.step0;
+        const int color = s ? sw.color1 : sw.color0;
         vs[k][lane] = make_uint2(cur.x, cur.z);
         __syncthreads();
         uint32_t vua = 0u, vub = 0u;
