@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -96,7 +97,9 @@ Stage &stage() {
 void pool_init(Stage &s) {
     if (!s.pool) {
         const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-        s.pool = new CopyPool((int)std::min(8u, std::max(1u, hc / 2)));
+        unsigned n = std::min(8u, std::max(1u, hc / 2));
+        if (const char *ev = getenv("TSB_COPY_THREADS")) n = (unsigned)std::max(1, atoi(ev));
+        s.pool = new CopyPool((int)n);
     }
 }
 
