@@ -368,14 +368,11 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
 // list with a grid stride; each thread's 16-byte slice of the tiles
 // kPipeStages-1 ahead is fetched with cp.async into the thread's own
 // shared-memory slots while the current tile is swept, so the HBM latency
-// of a tile overlaps the sweeps of the previous one (TSB_PIPE_STAGES=3 keeps
-// two tiles in flight: measured slower at C4, 63.0 vs 58.7 us per sweep).
+// of a tile overlaps the sweeps of the previous one (two tiles in flight
+// measured slower at C4, 63.0 vs 58.7 us per sweep).
 // A thread only ever reads the slot it filled itself, so
 // cp.async.wait_group needs no block barrier.
-#ifndef TSB_PIPE_STAGES
-#define TSB_PIPE_STAGES 2
-#endif
-constexpr int kPipeStages = TSB_PIPE_STAGES;
+constexpr int kPipeStages = 2;
 constexpr size_t kPipeSmem = kMSmem + kPipeStages * sizeof(uint4) * 32 * kMRows;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -394,7 +391,6 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t step0 = *c.step_dev + c.step;
-#if TSB_PIPE_STAGES == 2
     auto fetch = [&](int i, int b) {
         const int2 t = c.tiles[i];
         const int r = t.y * kMOut - kMK + k;
@@ -418,34 +414,6 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
         const int r = t.y * kMOut - kMK + k;
         multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
     }
-#else
-    // one commit group per stage, empty past the end of the list, so that
-    // "wait until at most kPipeStages-1 groups are pending" always means the
-    // current tile has landed
-    auto fetch = [&](int i, int b) {
-        if (i < c.ntiles) {
-            const int2 t = c.tiles[i];
-            const int r = t.y * kMOut - kMK + k;
-            uint4 *dst = slot + b * 32 * kMRows;
-            if (r >= 0 && r < c.side) cp_async16(dst, base + (ptrdiff_t)r * c.pitch + t.x + 2 * lane);
-            else *dst = make_uint4(0u, 0u, 0u, 0u);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-#pragma unroll
-    for (int st = 0; st < kPipeStages - 1; ++st) fetch((int)blockIdx.x + st * (int)gridDim.x, st);
-    int b = 0;
-    for (int i = blockIdx.x; i < c.ntiles; i += gridDim.x) {
-        fetch(i + (kPipeStages - 1) * (int)gridDim.x, (b + kPipeStages - 1) % kPipeStages);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");  // this tile's group has landed
-        const uint4 cur = slot[b * 32 * kMRows];
-        const int2 t = c.tiles[i];
-        const int r = t.y * kMOut - kMK + k;
-        multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
-        b = (b + 1) % kPipeStages;
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-#endif
 }
 
 // The same temporal blocking with ONE {V,H} word per lane (tiles of 30 output

@@ -4,15 +4,6 @@
 
 #include "tsb_internal.cuh"
 
-// build variants for A/B runs (tools/gpu_round2_*.sh): one queue loop per
-// (word, state-3) pair; the comparison x < t << 11 instead of (x >> 11) < t
-#ifndef TSB_QSPLIT
-#define TSB_QSPLIT 0
-#endif
-#ifndef TSB_CMP11
-#define TSB_CMP11 0
-#endif
-
 namespace tsb {
 
 // Heat-bath coins of a warp's rotateable active vertices, load-balanced.
@@ -43,16 +34,6 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int pos = incl - cnt;
     // job = is3 << 11 | lane << 6 | word << 5 | bit
-#if TSB_QSPLIT
-    {
-        const uint32_t qb = (uint32_t)lane << 6;
-        uint16_t *qp = queue + pos;
-        for (uint32_t m = ra & ia; m; m &= m - 1) *qp++ = (uint16_t)(qb | 0x800u | (uint32_t)(__ffs(m) - 1));
-        for (uint32_t m = ra & ~ia; m; m &= m - 1) *qp++ = (uint16_t)(qb | (uint32_t)(__ffs(m) - 1));
-        for (uint32_t m = rb & ib; m; m &= m - 1) *qp++ = (uint16_t)(qb | 0x820u | (uint32_t)(__ffs(m) - 1));
-        for (uint32_t m = rb & ~ib; m; m &= m - 1) *qp++ = (uint16_t)(qb | 0x20u | (uint32_t)(__ffs(m) - 1));
-    }
-#else
     for (uint32_t m = ra; m; m &= m - 1) {
         const int b = __ffs(m) - 1;
         queue[pos++] = (uint16_t)((((ia >> b) & 1u) << 11) | (lane << 6) | b);
@@ -61,7 +42,6 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
         const int b = __ffs(m) - 1;
         queue[pos++] = (uint16_t)((((ib >> b) & 1u) << 11) | (lane << 6) | 32 | b);
     }
-#endif
     fres[2 * lane] = 0u;
     fres[2 * lane + 1] = 0u;
     // pad the queue to a multiple of 32 with copies of job 0: a duplicate
@@ -69,12 +49,9 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     // loop below then runs two independent splitmix chains per lane without
     // a divergent tail (lanes of a warp issue together, so the padding costs
     // no issue slots)
-#ifndef TSB_FIRE_PAD
-#define TSB_FIRE_PAD 1
-#endif
-    const int padded = TSB_FIRE_PAD ? (total + 31) & ~31 : total;
+    const int padded = (total + 31) & ~31;
     __syncwarp();
-    if (TSB_FIRE_PAD && lane < padded - total) queue[total + lane] = queue[0];
+    if (lane < padded - total) queue[total + lane] = queue[0];
     __syncwarp();
     const uint64_t salt = (step + 1ull) * kGold;
     // site index i = r * side + column, column = 32 * (wa of lane 0) + col,
@@ -85,34 +62,26 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     auto col_of = [](uint32_t q) -> uint32_t {
         return WPL == 2 ? (q & 2047u) : (((q >> 6) & 31u) * (32u * WPL) + (q & 63u));
     };
-#if TSB_CMP11
-    const bool t_all = t >= (1ull << 53);
-    const uint64_t t11 = t_all ? ~0ull : t << 11;  // x < t << 11 <=> (x >> 11) < t
-#define TSB_BELOW(x, ts) (TM == 2 ? ((x) >> 11) < (ts) : (t_all || (x) < t11))
-#else
-#define TSB_BELOW(x, ts) (((x) >> 11) < (ts))
-#endif
     int j = lane;
     for (; j + 32 < padded; j += 64) {
-        const uint32_t q0 = queue[j], q1 = queue[j + 32];  // unpadded builds: j + 32 < total, both valid
+        const uint32_t q0 = queue[j], q1 = queue[j + 32];
         const uint32_t c0 = col_of(q0), c1 = col_of(q1);
         // two independent chains for ILP
-        const uint64_t x0 = mix64_hot(mix64_hot(kb + (uint64_t)c0 * kGold) + salt);
-        const uint64_t x1 = mix64_hot(mix64_hot(kb + (uint64_t)c1 * kGold) + salt);
+        const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
+        const uint64_t x1 = mix64(mix64(kb + (uint64_t)c1 * kGold) + salt);
         const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
         const uint64_t t1 = TM == 2 ? __ldg(tgrid + row_idx + c1) : t;
-        const bool f0 = TSB_BELOW(x0, t0) == (bool)(q0 >> 11), f1 = TSB_BELOW(x1, t1) == (bool)(q1 >> 11);
+        const bool f0 = ((x0 >> 11) < t0) == (bool)(q0 >> 11), f1 = ((x1 >> 11) < t1) == (bool)(q1 >> 11);
         // fire word of (lane', word) = fres[2 * lane' + word] (WPL = 1: word 0 only)
         if (f0) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
         if (f1) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
     }
     if (j < padded) {
         const uint32_t q0 = queue[j], c0 = col_of(q0);
-        const uint64_t x0 = mix64_hot(mix64_hot(kb + (uint64_t)c0 * kGold) + salt);
+        const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
         const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
-        if (TSB_BELOW(x0, t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+        if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
     }
-#undef TSB_BELOW
     __syncwarp();
     return make_uint2(fres[2 * lane], fres[2 * lane + 1]);
 }

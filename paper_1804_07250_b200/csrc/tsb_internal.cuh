@@ -30,29 +30,6 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-#ifndef TSB_MIX_BAL
-#define TSB_MIX_BAL 0
-#endif
-// z ^ (z >> s) with the shifts on the FMA pipe (IMAD.HI / IMAD) instead of
-// SHF on the ALU pipe: x >> s = hi32(x * 2^(32-s)); the two halves of the
-// 64-bit shift occupy disjoint bits, so their OR is a sum.  Same value as
-// the plain form, bit for bit.
-__device__ __forceinline__ uint64_t xorshift_fma(uint64_t z, int s) {
-    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32), m = 1u << (32 - s);
-    uint32_t shi, slo;
-    asm("mul.hi.u32 %0, %1, %2;" : "=r"(shi) : "r"(hi), "r"(m));
-    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(slo) : "r"(lo), "r"(m), "r"(hi * m));
-    return ((uint64_t)(hi ^ shi) << 32) | (uint64_t)(lo ^ slo);
-}
-
-// splitmix64 finaliser for the hot coin loops: the first TSB_MIX_BAL
-// xorshifts on the FMA pipe (pipe balance when the ALU pipe is the limiter).
-__device__ __forceinline__ uint64_t mix64_hot(uint64_t z) {
-    z = (TSB_MIX_BAL >= 1 ? xorshift_fma(z, 30) : (z ^ (z >> 30))) * kM1;
-    z = (TSB_MIX_BAL >= 2 ? xorshift_fma(z, 27) : (z ^ (z >> 27))) * kM2;
-    return z ^ (z >> 31);
-}
-
 // Per-family base key (rng.py:83).
 __host__ __device__ __forceinline__ uint64_t family_base(uint64_t seed) {
     return mix64(seed ^ kBaseXor);
