@@ -273,10 +273,9 @@ __device__ __forceinline__ uint32_t need_b(int s, int k, int lane) {
 template <int TM, int MODE>
 __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], uint2 (*fs)[32], uint32_t (*fres)[64],
                                            uint16_t (*queue)[1024], int k, int lane, int z, int r, int wa,
-                                           bool in_grid, uint4 cur, uint64_t step0) {
+                                           bool in_grid, uint4 cur, const Sweeps2 &sw) {
     const uint32_t act0 = (r & 1) ? 0xAAAAAAAAu : 0x55555555u;  // active sites of colour 0 (BLACK: r+c even)
     static_assert(kMK == 2, "two sweeps per launch");
-    const Sweeps2 sw = sweeps_of<MODE>(c, z, step0);
 #pragma unroll 1
     for (int s = 0; s < kMK; ++s) {
         if (!(s ? sw.on1 : sw.on0)) continue;  // block-uniform
@@ -359,7 +358,8 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c
     if (c.cost && threadIdx.x == 0) t_start = clock64();
     uint4 cur = make_uint4(0u, 0u, 0u, 0u);
     if (in_grid) cur = __ldg(reinterpret_cast<const uint4 *>(row + wa));
-    multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur, *c.step_dev + c.step);
+    multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, wa, in_grid, cur,
+                         sweeps_of<MODE>(c, z, *c.step_dev + c.step));
     if (c.cost && threadIdx.x == 0) c.cost[c.order[blockIdx.x]] = (unsigned)(clock64() - t_start);  // after the last barrier
     TT(5);
 }
@@ -390,29 +390,37 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
     const uint2 *base = c.src + (size_t)z * c.chain_stride;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t step0 = *c.step_dev + c.step;
-    auto fetch = [&](int i, int b) {
-        const int2 t = c.tiles[i];
+    // the launch's two sweeps (steps, colours, skip flags) are the same for
+    // every tile: resolved once per block
+    const Sweeps2 sw = sweeps_of<MODE>(c, z, *c.step_dev + c.step);
+    auto fetch = [&](int2 t, int b) {
         const int r = t.y * kMOut - kMK + k;
         uint4 *dst = slot + b * 32 * kMRows;
         if (r >= 0 && r < c.side) cp_async16(dst, base + (ptrdiff_t)r * c.pitch + t.x + 2 * lane);
         else *dst = make_uint4(0u, 0u, 0u, 0u);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    // tile coordinates are read two tiles ahead, so the list load's latency
+    // hides behind a tile's sweeps instead of stalling the next fetch
+    const int G = gridDim.x;
+    int2 t_cur = (int)blockIdx.x < c.ntiles ? c.tiles[blockIdx.x] : make_int2(0, 0);
+    int2 t_nxt = (int)blockIdx.x + G < c.ntiles ? c.tiles[blockIdx.x + G] : make_int2(0, 0);
     int b = 0;
-    if ((int)blockIdx.x < c.ntiles) fetch(blockIdx.x, 0);
-    for (int i = blockIdx.x; i < c.ntiles; i += gridDim.x, b ^= 1) {
-        const int nx = i + gridDim.x;
+    if ((int)blockIdx.x < c.ntiles) fetch(t_cur, 0);
+    for (int i = blockIdx.x; i < c.ntiles; i += G, b ^= 1) {
+        const int nx = i + G;
+        const int2 t_nn = nx + G < c.ntiles ? c.tiles[nx + G] : make_int2(0, 0);
         if (nx < c.ntiles) {
-            fetch(nx, b ^ 1);
+            fetch(t_nxt, b ^ 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's group has landed
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         const uint4 cur = slot[b * 32 * kMRows];
-        const int2 t = c.tiles[i];
-        const int r = t.y * kMOut - kMK + k;
-        multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t.x + 2 * lane, r >= 0 && r < c.side, cur, step0);
+        const int r = t_cur.y * kMOut - kMK + k;
+        multi_tile<TM, MODE>(c, vs, fs, fres, queue, k, lane, z, r, t_cur.x + 2 * lane, r >= 0 && r < c.side, cur, sw);
+        t_cur = t_nxt;
+        t_nxt = t_nn;
     }
 }
 
