@@ -43,7 +43,7 @@ constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per b
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
 constexpr size_t kPipeMinBytes = 96ull << 20;  // launches whose two state buffers exceed this use the pipelined kernel
-constexpr int kOrderThreads = 1024;     // adaptive dispatch order (order_kernel): one block
+constexpr int kOrderThreads = 1024;     // adaptive dispatch order (replay_tail_kernel): one block
 constexpr int kOrderClasses = 4;
 constexpr int kOrderPer = 8;            // tiles per thread: launches of more tiles use the pipelined kernel
 constexpr size_t kMSmem = 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64 + 2 * kMRows * 1024;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kResThreads, 1) domino_resident_kernel(ResCtx 
         const uint64_t step = c.step0 + s;
         const uint64_t salt = (step + 1ull) * kGold;
         const int color = (int)(mix64(gkey + salt) >> 63);  // BLACK iff u < 1/2 (sweeps.py:266-269)
-        // collapsed run (colors_kernel): the next sweep has the same colour
+        // collapsed run (color_entry): the next sweep has the same colour
         if (c.collapse && s + 1 < c.n_steps && (int)(mix64(gkey + salt + kGold) >> 63) == color) continue;
         const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
         for (int i0 = 0; i0 < items; i0 += blockDim.x) {  // warp-uniform trip count
@@ -682,26 +682,24 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx
     }
 }
 
-// Colours of the next kGraphSweeps sweeps of every chain (graph mode).
-// Colour of every sweep of a replay (bit 0) and, with run collapsing, a
-// skip flag (bit 1): a sweep whose successor in the same walk has the same
-// colour is skipped.  The domino move is a heat-bath update -- a rotateable
+// Colour tables (graph mode): the colour of every sweep of a replay (bit 0)
+// and, with run collapsing, a skip flag (bit 1): a sweep whose successor in
+// the same walk has the same colour is skipped.  The domino move is a heat-bath update -- a rotateable
 // vertex becomes 12 iff u < p_up and 3 otherwise, whatever its state
 // (_kernels.py:46-55) -- and while one colour is swept the other colour does
 // not move, so the rotateable set of that colour cannot change within a run
 // of equal colours and only the last sweep of the run decides the state.
 // Skipping the others gives the identical state (tests: every golden walk,
 // oracle walks, CFTP samples and traces, with TSB_DOM_COLLAPSE=0 and 1).
-// step_dev[0] = step of the replay's first sweep, step_dev[1] = end of the walk.
-__global__ void colors_kernel(const uint64_t *seedinfo, const uint64_t *step_dev, uint64_t offset,
-                              uint8_t *colors, int collapse) {
-    const int z = blockIdx.x, i = threadIdx.x;
-    const uint64_t step = step_dev[0] + offset + (uint64_t)i;
-    const uint64_t g = seedinfo[2 * z + 1];
+// color_entry: the table entry of `step` for a chain with global key g, the
+// colour bit and the skip bit (the next sweep of the walk, which ends at `end`, has
+// the same colour).  Tables of kGraphSweeps entries per chain are written by
+// set_walk_kernel (a walk's first replay) and replay_tail_kernel (the next).
+__device__ __forceinline__ uint8_t color_entry(uint64_t g, uint64_t step, uint64_t end, int collapse) {
     const int col = (int)(mix64(g + (step + 1ull) * kGold) >> 63);
     int skip = 0;
-    if (collapse && step + 1ull < step_dev[1]) skip = (int)(mix64(g + (step + 2ull) * kGold) >> 63) == col;
-    colors[z * kGraphSweeps + i] = (uint8_t)(col | (skip << 1));
+    if (collapse && step + 1ull < end) skip = (int)(mix64(g + (step + 2ull) * kGold) >> 63) == col;
+    return (uint8_t)(col | (skip << 1));
 }
 
 // --------------------------------------------------------------- codecs
@@ -930,7 +928,7 @@ static bool pipe_launch(const tsb_domino *h, int n) {
 }
 
 // Whole-domain launches of the one-block-per-tile kernel use the adaptive
-// dispatch order (order_kernel); TSB_DOM_ADAPT=0 keeps band-major order.
+// dispatch order (reorder_tiles); TSB_DOM_ADAPT=0 keeps band-major order.
 static bool adaptive_order(const tsb_domino *h, int n) {
     // row windows (strips) only with several waves of tiles: on the ~2-wave
     // windows of Aztec 4096 heavy-first was slower (1/4 window 4.3 -> 7.1 us)
@@ -1019,13 +1017,20 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
 }
 
 __global__ void set_step_kernel(uint64_t *step_dev, uint64_t v) { *step_dev = v; }
-__global__ void set_walk_kernel(uint64_t *step_dev, uint64_t step0, uint64_t end) {
-    step_dev[0] = step0;
-    step_dev[1] = end;
+// step_dev = {step0, end}; with a colour table, also the table of the
+// first kGraphSweeps steps (launched <<<chains, kGraphSweeps>>>)
+__global__ void set_walk_kernel(uint64_t *step_dev, uint64_t step0, uint64_t end, const uint64_t *seedinfo = nullptr,
+                                uint8_t *colors = nullptr, int collapse = 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        step_dev[0] = step0;
+        step_dev[1] = end;
+    }
+    if (colors)
+        colors[blockIdx.x * kGraphSweeps + threadIdx.x] =
+            color_entry(seedinfo[2 * blockIdx.x + 1], step0 + threadIdx.x, end, collapse);
 }
-__global__ void advance_step_kernel(uint64_t *step_dev, uint64_t by) { *step_dev += by; }
 
-// canonical (band-major) order of a window's tiles [0, n): order_kernel input state
+// canonical (band-major) order of a window's tiles [0, n): reorder_tiles input state
 __global__ void order_reset_kernel(const int2 *tiles, int n, int *order, int2 *perm, unsigned *cost) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1050,11 +1055,7 @@ __device__ __forceinline__ int cost_class(unsigned cost, int n, unsigned long lo
     return x > 6ull * tot ? 3 : x > 3ull * tot ? 2 : x > 2ull * tot ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *cost, const int2 *tiles, int n,
-                                                                const uint64_t *step_dev, int every, int *order,
-                                                                int2 *perm) {
-    // the heavy tiles move slowly: reorder on every `every`-th replay only
-    if ((*step_dev / kGraphSweeps) % (uint64_t)every != 0) return;
+__device__ __forceinline__ void reorder_tiles(const unsigned *cost, const int2 *tiles, int n, int *order, int2 *perm) {
     typedef cub::BlockReduce<unsigned long long, kOrderThreads> Reduce;
     typedef cub::BlockScan<int, kOrderThreads> Scan;
     __shared__ union {
@@ -1096,6 +1097,37 @@ __global__ void __launch_bounds__(kOrderThreads) order_kernel(const unsigned *co
     }
 }
 
+// Bookkeeping between graph replays, one launch instead of three: the
+// adaptive tile reorder when it is due (the heavy tiles move slowly: every
+// `every`-th replay), the replay counter advance, and the colour table of
+// the next replay (colour-table walks; set_walk_kernel fills the first).
+struct ReplayTail {
+    const unsigned *cost;  // adaptive order (nullptr: none)
+    const int2 *tiles;
+    int ntiles, every;
+    int *order;
+    int2 *perm;
+    uint64_t *counter;          // step_dev[0] (colour tables) or step_dev[2] (executed-sweep lists)
+    const uint64_t *step_dev;   // step_dev[1] = end of the walk
+    const uint64_t *seedinfo;
+    uint8_t *colors;            // nullptr for list replays
+    int nchains, collapse;
+};
+
+__global__ void __launch_bounds__(kOrderThreads) replay_tail_kernel(ReplayTail t) {
+    const uint64_t base = *t.counter;
+    if (t.cost && (base / kGraphSweeps) % (uint64_t)t.every == 0)  // block-uniform
+        reorder_tiles(t.cost, t.tiles, t.ntiles, t.order, t.perm);
+    if (threadIdx.x == 0) *t.counter = base + kGraphSweeps;
+    if (t.colors) {
+        const uint64_t end = t.step_dev[1];
+        for (int i = threadIdx.x; i < t.nchains * kGraphSweeps; i += blockDim.x) {
+            const int z = i / kGraphSweeps, j = i - z * kGraphSweeps;
+            t.colors[i] = color_entry(t.seedinfo[2 * z + 1], base + kGraphSweeps + (uint64_t)j, end, t.collapse);
+        }
+    }
+}
+
 // A CUDA graph of kGraphSweeps sweeps (even, so the buffers end where they
 // started) followed by `step += kGraphSweeps`; long walks replay it, which
 // removes the per-launch host overhead (the kernels read the step base from
@@ -1118,16 +1150,26 @@ int ensure_graph(tsb_domino *h, int chain0, int n, bool compact) {
     // compact replays take the next kGraphSweeps entries of the executed-sweep
     // lists (step_dev[2] advances); colour-table replays the next kGraphSweeps
     // steps (step_dev[0] advances)
-    uint64_t *counter = compact ? h->step_dev + 2 : h->step_dev;
-    if (!compact)
-        colors_kernel<<<n, kGraphSweeps, 0, h->cap_stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
+    // (the colour table of a replay is written by the previous replay's
+    // tail or by set_walk_kernel)
     static_assert(kGraphSweeps % (2 * kMK) == 0, "graph replays must end in the starting buffer");
     for (int i = 0; i < kGraphSweeps / kMK && !rc; ++i)
         rc = launch_multi(h, chain0, n, (uint64_t)(i * kMK), h->cap_stream, compact);
-    if (!rc && adaptive_order(h, n)) order_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(h->m_cost + h->win_m0, h->mtiles + h->win_m0, h->win_mn,
-                                                          counter, h->m_order_every, h->m_order + h->win_m0,
-                                                          h->m_perm + h->win_m0);
-    advance_step_kernel<<<1, 1, 0, h->cap_stream>>>(counter, (uint64_t)kGraphSweeps);
+    ReplayTail tail;
+    const bool adapt = adaptive_order(h, n);
+    tail.cost = adapt ? h->m_cost + h->win_m0 : nullptr;
+    tail.tiles = h->mtiles + h->win_m0;
+    tail.ntiles = h->win_mn;
+    tail.every = h->m_order_every;
+    tail.order = h->m_order + h->win_m0;
+    tail.perm = h->m_perm + h->win_m0;
+    tail.counter = compact ? h->step_dev + 2 : h->step_dev;
+    tail.step_dev = h->step_dev;
+    tail.seedinfo = h->seedinfo;
+    tail.colors = compact ? nullptr : h->colors;
+    tail.nchains = n;
+    tail.collapse = h->collapse;
+    if (!rc) replay_tail_kernel<<<1, kOrderThreads, 0, h->cap_stream>>>(tail);
     if (!rc && h->graph_tail) rc = h->graph_tail(h, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) {
@@ -1604,7 +1646,7 @@ __global__ void set_segment_kernel(uint64_t *step_dev, uint64_t step) {
 
 // Executed-sweep lists of a walk segment (run collapsing, host side): sweep i
 // of the segment is executed unless sweep i+1 of the same walk has the same
-// colour (colors_kernel explains why that is exact).  Entry = i | colour << 31.
+// colour (color_entry's comment explains why that is exact).  Entry = i | colour << 31.
 static int build_lists(tsb_domino *h, int n, uint64_t seg_step, uint64_t len, bool walk_end, uint32_t *list,
                        int *cnt) {
     const size_t pitch = h->xpitch;
@@ -1698,13 +1740,16 @@ int tsb::walk_steps(tsb_domino *h, int chain0, int n, uint64_t step0, uint64_t n
         return walk_compact(h, chain0, n, step0, n_steps);
     if (n_steps >= kGraphSweeps) {
         if ((rc = ensure_graph(h, chain0, n, false))) return rc;
-        set_walk_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
+        set_walk_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps, h->seedinfo,
+                                                         h->colors, h->collapse);
         TSB_CUDA(cudaGetLastError());
         for (; s + kGraphSweeps <= n_steps; s += kGraphSweeps) TSB_CUDA(cudaGraphLaunch(h->graph_exec, h->stream));
     }
     if (n_steps - s >= (uint64_t)kMK) {  // remainder: direct multi-sweep launches (step_dev = step0 + s)
-        if (s == 0) set_walk_kernel<<<1, 1, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps);
-        colors_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->seedinfo, h->step_dev, 0, h->colors, h->collapse);
+        // after replays the last replay's tail wrote this table
+        if (s == 0)
+            set_walk_kernel<<<n, kGraphSweeps, 0, h->stream>>>(h->step_dev, step0, step0 + n_steps, h->seedinfo,
+                                                             h->colors, h->collapse);
         TSB_CUDA(cudaGetLastError());
         for (uint64_t i = 0; s + kMK <= n_steps; s += kMK, i += kMK)
             if ((rc = launch_multi(h, chain0, n, i, h->stream, false))) return rc;

@@ -27,7 +27,7 @@ struct tsb_domino {
     int win_t0 = 0, win_tn = 0;   // swept tile range (row window; default all)
     int2 *mtiles = nullptr;       // tiles of the temporally blocked kernel (kMOut-row bands)
     int nmtiles = 0;
-    int *m_order = nullptr;       // dispatch order of whole-domain multi-sweep launches (order_kernel)
+    int *m_order = nullptr;       // dispatch order of whole-domain multi-sweep launches (replay_tail_kernel)
     unsigned *m_cost = nullptr;   // last block duration per multi-sweep tile (cycles)
     int2 *m_perm = nullptr;       // mtiles in that order
     bool m_adapt = true;          // TSB_DOM_ADAPT=0: band-major order
@@ -39,7 +39,7 @@ struct tsb_domino {
     int num_sms = 148;
     int m_wpl = 2;  // words per lane of the multi-sweep tiles (1: 30-word tiles for narrow lattices)
     bool coupled = false, g_coupled = false;  // chains 2j, 2j+1 share seeds (CFTP pairs): share the coins
-    int collapse = 1, g_collapse = -1;  // skip sweeps followed by a sweep of the same colour (colors_kernel)
+    int collapse = 1, g_collapse = -1;  // skip sweeps followed by a sweep of the same colour (color_entry)
     int g_compact = -1;
     // run-collapsed walks (walk_compact): executed-sweep lists per chain
     std::vector<uint64_t> gkeys;  // host copies of the pushed chains' global keys
