@@ -156,16 +156,16 @@ GRAPH_SWEEPS = 64  # sweeps per CUDA-graph replay (kGraphSweeps)
 
 
 def launches_per_walk(n: int) -> int:
-    """Kernels one tsb_domino_walk of n sweeps launches: set_step, then per
-    graph replay a colour kernel, GRAPH_SWEEPS/MK multi-sweep kernels, the
-    adaptive-order kernel (whole-domain walks; it returns at once on three
-    replays of four) and the step advance; the remainder as direct
-    multi-sweep launches (plus a colour kernel) and at most one single-sweep
-    kernel."""
+    """Kernels one tsb_domino_walk of n sweeps launches: set_walk (step base
+    and the first colour table), then per graph replay GRAPH_SWEEPS/MK
+    multi-sweep kernels and the replay tail (adaptive reorder when due, step
+    advance, next colour table); the remainder as direct multi-sweep
+    launches (after set_walk when there was no replay) and at most one
+    single-sweep kernel."""
     replays, rem = divmod(n, GRAPH_SWEEPS)
-    k = 1 + replays * (3 + GRAPH_SWEEPS // MK) if replays else 0
-    if rem >= MK:  # remainder: (set_step,) colour kernel, direct multi-sweep launches
-        k += (0 if replays else 1) + 1 + rem // MK
+    k = 1 + replays * (1 + GRAPH_SWEEPS // MK) if replays else 0
+    if rem >= MK:  # remainder: (set_walk,) direct multi-sweep launches
+        k += (0 if replays else 1) + rem // MK
         rem %= MK
     return k + rem
 
