@@ -39,7 +39,11 @@ namespace tsb {
 constexpr int kTileRows = 15;   // output rows per block tile (+1 halo fire row)
 constexpr int kTileWords = 62;  // output words per tile: 64 loaded (2 per lane), 1 halo word each side
 constexpr int kPad = 2;         // zero words left of every state row (lane 0's halo of the first tile)
-constexpr int kMRows = 16;      // rows per temporally blocked tile (warps per block)
+#ifndef TSB_MROWS
+#define TSB_MROWS 16
+#endif
+constexpr int kMRows = TSB_MROWS;  // rows per temporally blocked tile (warps per block)
+constexpr int kMBlocks = 48 / kMRows;  // resident blocks per SM (48 warps)
 constexpr int kMK = 2;          // sweeps per temporally blocked launch
 constexpr int kMOut = kMRows - 2 * kMK;  // exact output rows per temporally blocked tile
 constexpr size_t kPipeMinBytes = 96ull << 20;  // launches whose two state buffers exceed this use the pipelined kernel
@@ -339,7 +343,7 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
         reinterpret_cast<uint16_t(*)[1024]>(dsm + 2 * sizeof(uint2) * kMRows * 32 + sizeof(uint32_t) * kMRows * 64)
 
 template <int TM, int MODE>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi_kernel(SweepCtx c) {
     TT(0);
     MULTI_SMEM;
     __shared__ long long t_start;
@@ -381,7 +385,7 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 
 template <int TM, int MODE>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi_pipe_kernel(SweepCtx c) {
     MULTI_SMEM;
     uint4 *slot = reinterpret_cast<uint4 *>(dsm + kMSmem) + threadIdx.x;  // [kPipeStages][blockDim]
     const int lane = threadIdx.x & 31;
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(32 * kMRows, 3) domino_multi_pipe_kernel(Sweep
 // where the 62-word tiles would leave half of every warp outside the domain.
 // Lanes 0 and 31 hold the halo words.
 template <int TM, int MODE>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi1_kernel(SweepCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t(*vs)[32] = reinterpret_cast<uint32_t(*)[32]>(dsm);
     uint32_t(*fs)[32] = reinterpret_cast<uint32_t(*)[32]>(dsm + sizeof(uint2) * kMRows * 32);
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(kResThreads, 1) domino_resident_kernel(ResCtx 
 // it is rotateable there and c equals its "state 3" bit -- exactly what two
 // independent sweeps compute.  Narrow (1 word per lane) tiles.
 template <int TM, int MODE>
-__global__ void __launch_bounds__(32 * kMRows, 3) domino_multi1c_kernel(SweepCtx c) {
+__global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi1c_kernel(SweepCtx c) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t(*vs)[kMRows][32] = reinterpret_cast<uint32_t(*)[kMRows][32]>(dsm);
     uint32_t(*fs)[kMRows][32] = reinterpret_cast<uint32_t(*)[kMRows][32]>(dsm + 2 * sizeof(uint32_t) * kMRows * 32);
@@ -1006,7 +1010,7 @@ int launch_multi(tsb_domino *h, int chain0, int n, uint64_t step_off, cudaStream
     }
     // HBM-streaming launches: the persistent cp.async-pipelined kernel (pipe_launch)
     if (pipe_launch(h, n)) {
-        cfg.gridDim.x = std::min(h->win_mn, 3 * h->num_sms);
+        cfg.gridDim.x = std::min(h->win_mn, kMBlocks * h->num_sms);
         cfg.dynamicSmemBytes = kPipeSmem;
         TSB_DOM_LAUNCH(domino_multi_pipe_kernel);
         return TSB_OK;
@@ -1229,7 +1233,7 @@ int tsb_domino_create_window(int device, int side, int row_lo, int row_hi, const
 // Rows beyond a window that its tiles may load or store: a multi-sweep tile
 // reaches kMK + kMOut - 1 rows past the window edge, a single-sweep tile
 // kTileRows (zero there: the stale halo a strip never reads back).
-constexpr int kWinMargin = 16;
+constexpr int kWinMargin = kMK + kMOut - 1 > 16 ? kMK + kMOut - 1 : 16;
 
 static int create_impl(int device, int side, int nchains, const uint8_t *faces, int row_lo, int row_hi,
                        tsb_domino **out) {
