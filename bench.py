@@ -340,7 +340,7 @@ def relaunch_under_torchrun(args) -> int:
 
 def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dist, seed, collapse=False):
     """The same step timed from the committed warm state instead of T_max
-    (bench_data/aztec4096_warm.npz: T_max + 2^24 sweeps, ~10 % of vertices
+    (bench_data/aztec4096_warm.npz: T_max + 4 n^2 sweeps, ~11 % of vertices
     rotateable, i.e. the regime a sampler spends its life in; the frozen T_max
     start has 0.3 %).  Device events per step, L2 flushed between steps."""
     sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -387,8 +387,8 @@ def warm_record(args, d, plan, counts, stream, flush, red_dev, world, torch, dis
             "ms_per_step": float(t.item()) / args.steps, "us_per_sweep": 1e3 * float(t.item()) / (args.steps * S),
             "rotateable_frac_end": rot,
             "roofline": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
-            "state": "bench_data/aztec4096_warm.npz (T_max + 2^24 sweeps of seed 0xA11CE, sha "
-                     + str(np.load(path)["sha"]) + ")"}
+            "state": "bench_data/aztec4096_warm.npz (T_max + %d sweeps of seed 0xA11CE, sha %s)"
+                     % (int(np.load(path)["sweeps"]), str(np.load(path)["sha"]))}
 
 
 def collapsed_record(args, d, plan, t_max, counts, stream, flush, red_dev, world, torch, dist, seed):
