@@ -62,25 +62,36 @@ __device__ __noinline__ uint2 warp_fire(uint32_t ra, uint32_t rb, uint32_t ia, u
     auto col_of = [](uint32_t q) -> uint32_t {
         return WPL == 2 ? (q & 2047u) : (((q >> 6) & 31u) * (32u * WPL) + (q & 63u));
     };
-    int j = lane;
-    for (; j + 32 < padded; j += 64) {
-        const uint32_t q0 = queue[j], q1 = queue[j + 32];
-        const uint32_t c0 = col_of(q0), c1 = col_of(q1);
-        // two independent chains for ILP
-        const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
-        const uint64_t x1 = mix64(mix64(kb + (uint64_t)c1 * kGold) + salt);
-        const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
-        const uint64_t t1 = TM == 2 ? __ldg(tgrid + row_idx + c1) : t;
-        const bool f0 = ((x0 >> 11) < t0) == (bool)(q0 >> 11), f1 = ((x1 >> 11) < t1) == (bool)(q1 >> 11);
-        // fire word of (lane', word) = fres[2 * lane' + word] (WPL = 1: word 0 only)
-        if (f0) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
-        if (f1) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
-    }
-    if (j < padded) {
-        const uint32_t q0 = queue[j], c0 = col_of(q0);
-        const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
-        const uint64_t t0 = TM == 2 ? __ldg(tgrid + row_idx + c0) : t;
-        if (((x0 >> 11) < t0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+    // below(x, col): the draw's u < p for the site in column col
+    auto deal = [&](auto below) {
+        int j = lane;
+        for (; j + 32 < padded; j += 64) {
+            const uint32_t q0 = queue[j], q1 = queue[j + 32];
+            const uint32_t c0 = col_of(q0), c1 = col_of(q1);
+            // two independent chains for ILP
+            const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
+            const uint64_t x1 = mix64(mix64(kb + (uint64_t)c1 * kGold) + salt);
+            const bool f0 = below(x0, c0) == (bool)(q0 >> 11), f1 = below(x1, c1) == (bool)(q1 >> 11);
+            // fire word of (lane', word) = fres[2 * lane' + word] (WPL = 1: word 0 only)
+            if (f0) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+            if (f1) atomicOr(&fres[(q1 >> 5) & 63u], 1u << (q1 & 31u));
+        }
+        if (j < padded) {
+            const uint32_t q0 = queue[j], c0 = col_of(q0);
+            const uint64_t x0 = mix64(mix64(kb + (uint64_t)c0 * kGold) + salt);
+            if (below(x0, c0) == (bool)(q0 >> 11)) atomicOr(&fres[(q0 >> 5) & 63u], 1u << (q0 & 31u));
+        }
+    };
+    if (TM == 0 && t == (1ull << 52)) {
+        // p = 1/2 (uniform weights): (x >> 11) < 2^52 iff bit 63 of x is 0,
+        // which the compiler reads off the last multiply (no final xorshift
+        // or 64-bit compare)
+        deal([](uint64_t x, uint32_t) { return (int32_t)(uint32_t)(x >> 32) >= 0; });
+    } else {
+        deal([&](uint64_t x, uint32_t c) {
+            const uint64_t tt = TM == 2 ? __ldg(tgrid + row_idx + c) : t;
+            return (x >> 11) < tt;
+        });
     }
     __syncwarp();
     return make_uint2(fres[2 * lane], fres[2 * lane + 1]);
