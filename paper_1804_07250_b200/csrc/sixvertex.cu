@@ -172,6 +172,7 @@ struct SvMCtx {
     int n, f, W, pitch;
     int K, out_rows;      // sweeps per launch, exact rows per tile (2*NW - 2K)
     int collapse;         // skip sweeps followed by a sweep of the same class
+    int half;             // every LUT entry is 2^52 (p_high = 1/2: a = b = c)
     int stride, woff;     // column tiles: first word of tile x = x*stride + woff
     uint64_t step;        // offset of this launch inside the graph replay
     uint64_t lut[32];
@@ -318,19 +319,26 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
             const uint64_t salt = (step0 + (uint64_t)s + 1ull) * kGold;
             // site index R * f + 32 * (word) + bit, word = wl(lane 0) + lane' * WPL + j
             const uint64_t row_idx = (uint64_t)R * (uint64_t)c.f + (uint64_t)(int64_t)((wl - lane * WPL) * 32);
-            for (int q = lane; q < total; q += 64) {
-                const bool two = q + 32 < total;
-                const uint32_t j0 = queue[q], j1 = two ? queue[q + 32] : j0;
-                const uint32_t w0 = ((j0 >> 6) & 31u) * WPL + ((j0 >> 4) & 3u), b0 = ((j0 & 15u) << 1) | (uint32_t)pc;
-                const uint32_t w1 = ((j1 >> 6) & 31u) * WPL + ((j1 >> 4) & 3u), b1 = ((j1 & 15u) << 1) | (uint32_t)pc;
-                const uint64_t i0 = row_idx + (uint64_t)(w0 * 32u + b0);
-                const uint64_t i1 = row_idx + (uint64_t)(w1 * 32u + b1);
-                const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
-                const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
-                // local min (up) moves iff u < p_high; local max moves iff u >= p_high
-                if (((x0 >> 11) < lut[j0 >> 11]) == !((j0 >> 15) & 1u)) atomicOr(&fres[w0], 1u << b0);
-                if (two && ((x1 >> 11) < lut[j1 >> 11]) == !((j1 >> 15) & 1u)) atomicOr(&fres[w1], 1u << b1);
-            }
+            // high(x, job): u < p_high for the job's LUT entry
+            auto deal = [&](auto high) {
+                for (int q = lane; q < total; q += 64) {
+                    const bool two = q + 32 < total;
+                    const uint32_t j0 = queue[q], j1 = two ? queue[q + 32] : j0;
+                    const uint32_t w0 = ((j0 >> 6) & 31u) * WPL + ((j0 >> 4) & 3u), b0 = ((j0 & 15u) << 1) | (uint32_t)pc;
+                    const uint32_t w1 = ((j1 >> 6) & 31u) * WPL + ((j1 >> 4) & 3u), b1 = ((j1 & 15u) << 1) | (uint32_t)pc;
+                    const uint64_t i0 = row_idx + (uint64_t)(w0 * 32u + b0);
+                    const uint64_t i1 = row_idx + (uint64_t)(w1 * 32u + b1);
+                    const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
+                    const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
+                    // local min (up) moves iff u < p_high; local max moves iff u >= p_high
+                    if (high(x0, j0) == !((j0 >> 15) & 1u)) atomicOr(&fres[w0], 1u << b0);
+                    if (two && high(x1, j1) == !((j1 >> 15) & 1u)) atomicOr(&fres[w1], 1u << b1);
+                }
+            };
+            if (c.half)  // p_high = 1/2: (x >> 11) < 2^52 iff bit 63 of x is 0
+                deal([](uint64_t x, uint32_t) { return (int32_t)(uint32_t)(x >> 32) >= 0; });
+            else
+                deal([&](uint64_t x, uint32_t j) { return (x >> 11) < lut[j >> 11]; });
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < WPL; ++j) {
@@ -603,7 +611,11 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
     c.stride = h->m_stride;
     c.woff = h->m_woff;
     c.step = step_off;
-    for (int i = 0; i < 32; ++i) c.lut[i] = h->lut[i];
+    c.half = 1;
+    for (int i = 0; i < 32; ++i) {
+        c.lut[i] = h->lut[i];
+        c.half &= h->lut[i] == (1ull << 52);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->m_gx, (h->f + c.out_rows - 1) / c.out_rows, n);
     cfg.stream = stream;
