@@ -393,3 +393,40 @@ def test_adaptive_order_with_per_site_thresholds(monkeypatch, weights):
     seeds = np.array([1, 2, 3], dtype=np.uint64)
     out = ts.random_walk_batch(start, seeds, 530, plan)
     assert np.array_equal(out, oracle.domino_walk(start, seeds, plan.p_up, 530))
+
+
+def test_bench_launch_count_matches_profiler():
+    """bench.py's `gpu_launches` claim: the kernels one 1000-sweep walk of the
+    headline workload launches (set_walk, 15 graph replays of 32 multi-sweep
+    kernels + the replay tail, 20 remainder multi-sweep kernels), counted by
+    the CUDA profiler (CUPTI activity records include graph kernel nodes)."""
+    import sys
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1804_07250_b200.lattice import aztec_extremal_states
+
+    order = 4096  # bench.py's workload: whole-domain tiles with the adaptive order
+    d = ts.Domain.aztec(order)
+    h = DominoHandle(d, d.n + 1, 1)
+    h.set_collapse(False)
+    h.set_plan(ts.SweepPlan(d))
+    h.upload(aztec_extremal_states(order)[0][None])
+    h.walk([5], 1000)  # graphs captured outside the profiled walk
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        h.walk([5], 1000, step0=1000)
+        h.sync()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    ours = [n for n in names if "tsb::" in n or "domino" in n or "replay_tail" in n or "set_walk" in n]
+    assert len(ours) == bench.launches_per_walk(1000), collections_summary(ours)
+
+
+def collections_summary(names):
+    import collections
+
+    return dict(collections.Counter(n.split("(")[0] for n in names))
