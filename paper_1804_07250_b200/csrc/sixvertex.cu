@@ -257,12 +257,9 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
                 d[j] = i + 1 < TR ? rows[i + 1][lane * WPL + j] : 0u;
             }
         }
-        uint32_t uL = __shfl_up_sync(0xffffffffu, u[WPL - 1], 1), bL = __shfl_up_sync(0xffffffffu, b[WPL - 1], 1),
-                 dL = __shfl_up_sync(0xffffffffu, d[WPL - 1], 1);
-        uint32_t uR = __shfl_down_sync(0xffffffffu, u[0], 1), bR = __shfl_down_sync(0xffffffffu, b[0], 1),
-                 dR = __shfl_down_sync(0xffffffffu, d[0], 1);
-        if (lane == 0) uL = bL = dL = 0u;
-        if (lane == 31) uR = bR = dR = 0u;
+        uint32_t bL = __shfl_up_sync(0xffffffffu, b[WPL - 1], 1), bR = __shfl_down_sync(0xffffffffu, b[0], 1);
+        if (lane == 0) bL = 0u;
+        if (lane == 31) bR = 0u;
         // coins that cannot reach a stored face are not drawn: a flip moves
         // one row / column per sweep, so sweep s only needs tile rows
         // s+1 .. TR-2-s and, in tiles with word halos, the halo bits within
@@ -273,27 +270,42 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
         const uint32_t hmask_r = c.woff < 0 && lane == 31 ? (reach >= 32 ? ~0u : (1u << reach) - 1u) : ~0u;
         const int odd = (pr + pc + p0) & 1;  // parity of the class faces
         const uint32_t pcm = pc ? 0xAAAAAAAAu : 0x55555555u;
-        uint32_t mn[WPL], cand[WPL], nw[WPL], ne[WPL], sw[WPL], se[WPL];
+        // candidates (local minima and maxima) first; the rest of the fire
+        // test -- which kind, the diagonal faces -- only in warps that have
+        // candidates (the frozen bulk of an early state pays the masks alone)
+        uint32_t alleq[WPL], cand[WPL];
         int cnt = 0;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const uint32_t pb = j > 0 ? b[j - 1] : bL, nb = j < WPL - 1 ? b[j + 1] : bR;
-            const uint32_t pu = j > 0 ? u[j - 1] : uL, nu = j < WPL - 1 ? u[j + 1] : uR;
-            const uint32_t pd = j > 0 ? d[j - 1] : dL, nd = j < WPL - 1 ? d[j + 1] : dR;
             const uint32_t left = (b[j] << 1) | (pb >> 31), right = (b[j] >> 1) | (nb << 31);
             const uint32_t eq_u = ~(u[j] ^ b[j]), eq_d = ~(d[j] ^ b[j]), eq_l = ~(left ^ b[j]),
                            eq_r = ~(right ^ b[j]);
-            const uint32_t all_eq = eq_u & eq_d & eq_l & eq_r, all_ne = ~(eq_u | eq_d | eq_l | eq_r);
+            alleq[j] = eq_u & eq_d & eq_l & eq_r;
+            const uint32_t all_ne = ~(eq_u | eq_d | eq_l | eq_r);
             const uint32_t act = rowok ? (cm[j] & pcm & (j == 0 ? hmask_l : ~0u) & (j == WPL - 1 ? hmask_r : ~0u)) : 0u;
-            mn[j] = (odd ? all_ne : all_eq) & act;
-            cand[j] = mn[j] | ((odd ? all_eq : all_ne) & act);
-            nw[j] = ((u[j] << 1) | (pu >> 31)) ^ b[j];
-            ne[j] = ((u[j] >> 1) | (nu << 31)) ^ b[j];
-            sw[j] = ((d[j] << 1) | (pd >> 31)) ^ b[j];
-            se[j] = ((d[j] >> 1) | (nd << 31)) ^ b[j];
+            cand[j] = (alleq[j] | all_ne) & act;
             cnt += __popc(cand[j]);
         }
         if (__any_sync(0xffffffffu, cnt != 0)) {
+            uint32_t uL = __shfl_up_sync(0xffffffffu, u[WPL - 1], 1), dL = __shfl_up_sync(0xffffffffu, d[WPL - 1], 1);
+            uint32_t uR = __shfl_down_sync(0xffffffffu, u[0], 1), dR = __shfl_down_sync(0xffffffffu, d[0], 1);
+            if (lane == 0) uL = dL = 0u;
+            if (lane == 31) uR = dR = 0u;
+            // local minima (all four neighbours one up): all equal for odd-parity
+            // class faces, all different for even ones; diagonal faces differ
+            // from the centre (by +-2) iff their bit differs
+            uint32_t mn[WPL], nw[WPL], ne[WPL], sw[WPL], se[WPL];
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+                const uint32_t pu = j > 0 ? u[j - 1] : uL, nu = j < WPL - 1 ? u[j + 1] : uR;
+                const uint32_t pd = j > 0 ? d[j - 1] : dL, nd = j < WPL - 1 ? d[j + 1] : dR;
+                mn[j] = odd ? cand[j] & ~alleq[j] : cand[j] & alleq[j];
+                nw[j] = ((u[j] << 1) | (pu >> 31)) ^ b[j];
+                ne[j] = ((u[j] >> 1) | (nu << 31)) ^ b[j];
+                sw[j] = ((d[j] << 1) | (pd >> 31)) ^ b[j];
+                se[j] = ((d[j] >> 1) | (nd << 31)) ^ b[j];
+            }
             int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
