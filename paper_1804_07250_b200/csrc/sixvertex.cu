@@ -48,6 +48,7 @@ struct tsb_sv {
     uint32_t *bits2 = nullptr;  // second buffer (out-of-place launches)
     uint64_t *step_dev = nullptr;
     int m_wpl = 1, m_nw = 8, m_K = 4, m_out = 8, m_stride = 32, m_woff = 0, m_gx = 1, m_gy = 1;
+    int m_xw = 0;  // tiles of 32 * m_wpl words plus the read-only east boundary word
     bool m_k_fixed = false;  // TSB_SV_K given: no per-batch choice of K
     int m_sms = 148;
     size_t m_smem = 0;
@@ -173,6 +174,7 @@ struct SvMCtx {
     int K, out_rows;      // sweeps per launch, exact rows per tile (2*NW - 2K)
     int collapse;         // skip sweeps followed by a sweep of the same class
     int half;             // every LUT entry is 2^52 (p_high = 1/2: a = b = c)
+    int xw;               // word 32 * WPL holds only the east boundary column: lane 31 keeps it read-only
     int stride, woff;     // column tiles: first word of tile x = x*stride + woff
     uint64_t step;        // offset of this launch inside the graph replay
     uint64_t lut[32];
@@ -180,21 +182,22 @@ struct SvMCtx {
 
 template <int WPL, int NW>
 constexpr size_t sv_multi_smem() {
-    return sizeof(uint32_t) * (2 * NW) * (32 * WPL)    // rows
+    return sizeof(uint32_t) * (2 * NW) * (32 * WPL + 1)  // rows (+ the east boundary word, XW tiles)
            + sizeof(uint64_t) * 32                      // lut
            + sizeof(uint32_t) * NW * (32 * WPL)         // per-warp flip words
            + sizeof(uint16_t) * NW * (32 * WPL) * 16;   // per-warp job queues
 }
 
-template <int WPL, int NW, int MINB = 1>
+// XW: tiles of 32 * WPL words plus the read-only east boundary word (c.xw)
+template <int WPL, int NW, int MINB = 1, bool XW = false>
 __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
-    constexpr int TW = 32 * WPL, TR = 2 * NW;
+    constexpr int TW = 32 * WPL, TR = 2 * NW, RS = TW + (XW ? 1 : 0);  // RS: smem row stride
     extern __shared__ __align__(16) unsigned char dsm[];
-    uint32_t(*rows)[TW] = reinterpret_cast<uint32_t(*)[TW]>(dsm);
-    uint64_t *lut = reinterpret_cast<uint64_t *>(dsm + sizeof(uint32_t) * TR * TW);
-    uint32_t *fres = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32) +
+    uint32_t(*rows)[RS] = reinterpret_cast<uint32_t(*)[RS]>(dsm);
+    uint64_t *lut = reinterpret_cast<uint64_t *>(dsm + sizeof(uint32_t) * TR * RS);
+    uint32_t *fres = reinterpret_cast<uint32_t *>(dsm + sizeof(uint32_t) * TR * RS + sizeof(uint64_t) * 32) +
                      (threadIdx.x >> 5) * TW;
-    uint16_t *queue = reinterpret_cast<uint16_t *>(dsm + sizeof(uint32_t) * TR * TW + sizeof(uint64_t) * 32 +
+    uint16_t *queue = reinterpret_cast<uint16_t *>(dsm + sizeof(uint32_t) * TR * RS + sizeof(uint64_t) * 32 +
                                                    sizeof(uint32_t) * NW * TW) +
                       (threadIdx.x >> 5) * TW * 16;
     const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
@@ -232,6 +235,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
         rows[2 * k][lane * WPL + j] = ra[j];
         rows[2 * k + 1][lane * WPL + j] = rb[j];
     }
+    // the east boundary word (tiles of W = 32 * WPL + 1 words whose last word
+    // holds only column n): never updated, read as the right neighbour of
+    // lane 31's last word and stored back unchanged
+    uint32_t xa = 0u, xb = 0u;
+    if (XW && lane == 31) {
+        xa = (Ra >= 0 && Ra < c.f) ? __ldcg(src + (size_t)Ra * c.pitch + TW) : 0u;
+        xb = (Ra + 1 >= 0 && Ra + 1 < c.f) ? __ldcg(src + (size_t)(Ra + 1) * c.pitch + TW) : 0u;
+        rows[2 * k][RS - 1] = xa;
+        rows[2 * k + 1][RS - 1] = xb;
+    }
     __syncthreads();
 #pragma unroll 1
     for (int s = 0; s < c.K; ++s) {
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
         }
         uint32_t bL = __shfl_up_sync(0xffffffffu, b[WPL - 1], 1), bR = __shfl_down_sync(0xffffffffu, b[0], 1);
         if (lane == 0) bL = 0u;
-        if (lane == 31) bR = 0u;
+        if (lane == 31) bR = XW ? (pr == 0 ? xa : xb) : 0u;
         // coins that cannot reach a stored face are not drawn: a flip moves
         // one row / column per sweep, so sweep s only needs tile rows
         // s+1 .. TR-2-s and, in tiles with word halos, the halo bits within
@@ -291,7 +304,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
             uint32_t uL = __shfl_up_sync(0xffffffffu, u[WPL - 1], 1), dL = __shfl_up_sync(0xffffffffu, d[WPL - 1], 1);
             uint32_t uR = __shfl_down_sync(0xffffffffu, u[0], 1), dR = __shfl_down_sync(0xffffffffu, d[0], 1);
             if (lane == 0) uL = dL = 0u;
-            if (lane == 31) uR = dR = 0u;
+            if (lane == 31) {
+                uR = XW && i > 0 ? rows[i - 1][RS - 1] : 0u;
+                dR = XW && i + 1 < TR ? rows[i + 1][RS - 1] : 0u;
+            }
             // local minima (all four neighbours one up): all equal for odd-parity
             // class faces, all different for even ones; diagonal faces differ
             // from the centre (by +-2) iff their bit differs
@@ -374,6 +390,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
         if (2 * k >= c.K && 2 * k < TR - c.K && Ra < c.f && Ra >= 0) dst[(size_t)Ra * c.pitch + w] = ra[j];
         if (2 * k + 1 >= c.K && 2 * k + 1 < TR - c.K && Ra + 1 < c.f && Ra + 1 >= 0)
             dst[(size_t)(Ra + 1) * c.pitch + w] = rb[j];
+    }
+    if (XW && lane == 31) {
+        if (2 * k >= c.K && 2 * k < TR - c.K && Ra < c.f && Ra >= 0) dst[(size_t)Ra * c.pitch + TW] = xa;
+        if (2 * k + 1 >= c.K && 2 * k + 1 < TR - c.K && Ra + 1 < c.f && Ra + 1 >= 0)
+            dst[(size_t)(Ra + 1) * c.pitch + TW] = xb;
     }
 }
 
@@ -522,6 +543,11 @@ constexpr int kSvGraphSweeps = 128;  // sweeps per graph replay
 // 4 words per lane with a one-word halo on each side.  K sweeps per launch
 // (even, dividing kSvGraphSweeps with an even number of launches per replay)
 // and NW warps per block; TSB_SV_K / TSB_SV_NW override them for tuning.
+static int getenv_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 void sv_multi_config(tsb_sv *h) {
     int force = 0;
     if (const char *e = getenv("TSB_SV_WPL")) force = atoi(e);
@@ -530,6 +556,15 @@ void sv_multi_config(tsb_sv *h) {
         h->m_woff = -1;
         h->m_stride = 32 * force - 2;
         h->m_gx = (h->W + h->m_stride - 1) / h->m_stride;
+    } else if (h->W <= 129 && h->W % 32 == 1 && h->n % 32 == 0 && getenv_int("TSB_SV_XW", 1)) {
+        // the last word holds only the east boundary column n (bit 0 of word
+        // n / 32): 32 * WPL words per row on 32 lanes, the boundary word read-only
+        // (DWBC 2048: 2 words per lane instead of 3 on 22 lanes)
+        h->m_wpl = (h->W - 1) / 32;
+        h->m_xw = 1;
+        h->m_woff = 0;
+        h->m_stride = 32 * h->m_wpl;
+        h->m_gx = 1;
     } else if (h->W <= 128) {
         h->m_wpl = (h->W + 31) / 32;
         h->m_woff = 0;
@@ -593,14 +628,13 @@ static int sv_launch_multi_t(const cudaLaunchConfig_t &cfg0, const SvMCtx &c, in
         return ev ? atoi(ev) : -1;
     }();
     const bool dense = NW == 16 && (dense_env >= 0 ? dense_env == 1 : blocks > 4 * (size_t)sms);
-    if (dense) {
-        TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
-        TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW, 2>, c));
+    auto go = [&](auto kern) -> int {
+        TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
+        TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, c));
         return TSB_OK;
-    }
-    TSB_CUDA(cudaFuncSetAttribute(sv_multi_kernel<WPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
-    TSB_CUDA(cudaLaunchKernelEx(&cfg, sv_multi_kernel<WPL, NW>, c));
-    return TSB_OK;
+    };
+    if (c.xw) return dense ? go(sv_multi_kernel<WPL, NW, 2, true>) : go(sv_multi_kernel<WPL, NW, 1, true>);
+    return dense ? go(sv_multi_kernel<WPL, NW, 2>) : go(sv_multi_kernel<WPL, NW>);
 }
 
 // One temporally blocked launch (m_K sweeps) of chains [chain0, chain0+n).
@@ -622,6 +656,7 @@ static int sv_launch_multi(tsb_sv *h, int chain0, int n, uint64_t step_off, cons
     c.out_rows = 2 * h->m_nw - 2 * c.K;
     c.stride = h->m_stride;
     c.woff = h->m_woff;
+    c.xw = h->m_xw;
     c.step = step_off;
     c.half = 1;
     for (int i = 0; i < 32; ++i) {
