@@ -205,3 +205,20 @@ def test_general_boundaries_golden():
         res = ts.sv_cftp(b.n, b, w, c["master"], count=3, trace=trace)
         assert np.array_equal(np.stack([ts.heights_from_config(x).heights for x in res]), g[f"c{j}_h"]), j
         assert trace.collapsed_at == c["collapsed_at"]
+
+
+@pytest.mark.parametrize("n,chains,steps", [(1024, 2, 60), (3072, 2, 36), (4096, 1, 30), (1024, 16, 40)])
+def test_east_boundary_word_tiles(n, chains, steps):
+    """n a multiple of 1024: rows of 32*WPL words plus the read-only east
+    boundary word (WPL = 1, 3, 4; 16 chains take the 2-blocks-per-SM build)
+    are bit-identical to the oracle."""
+    hi, lo = closed_form(n)
+    start = np.stack([lo if k % 2 == 0 else hi for k in range(chains)]).astype(np.int32)
+    seeds = np.arange(31, 31 + chains, dtype=np.uint64)
+    w = ts.SVWeights(1.0, 1.0, 1.0)
+    h = SixVertexHandle(n, chains)
+    h.set_weights(w)
+    h.upload(start)
+    h.walk(seeds, steps)
+    out = h.download()
+    assert np.array_equal(out, oracle.sv_walk(start, seeds, w.table(), steps))
