@@ -232,6 +232,10 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
     const int2 tile = c.tiles[blockIdx.x];
     const int x = tile.y * c.out_rows - c.K + k;
     const int wa = tile.x + 2 * lane, wb = wa + 1;  // band-aligned tile: tile.x = first loaded word (even)
+    // a halo word whose outer neighbour lies beyond the grid reads the true
+    // (zero) neighbour and stays exact: a tile starting at word 0 also owns
+    // word 0, one reaching the grid's last word also owns word tile.x + 63
+    const bool lclosed = tile.x == 0, rclosed = tile.x + 63 >= c.W - 1;
     const int z = blockIdx.z;
     const uint64_t gkey = c.seedinfo[2 * z + 1];
     const bool in_grid = x >= 0 && x < c.X;
@@ -275,8 +279,9 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         // within K-s (+1) columns of the interior
         const bool need = k >= s + 1 && k <= kLzMRows - 1 - s;
         const int reach = c.K - s;
-        const uint32_t hl = lane == 0 ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
-        const uint32_t hr = lane == 31 ? (reach >= 31 ? ~0u : (1u << (reach + 1)) - 1u) : ~0u;
+        // (a tile side closed by the grid edge has no stale halo: all its bits count)
+        const uint32_t hl = lane == 0 && !lclosed ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
+        const uint32_t hr = lane == 31 && !rclosed ? (reach >= 31 ? ~0u : (1u << (reach + 1)) - 1u) : ~0u;
         const uint32_t rota = need ? (lowa | higha) & mod3_mask((b3a - cls + 3) % 3) & hl : 0u;
         const uint32_t rotb = need ? (lowb | highb) & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
         uint2 f = make_uint2(0u, 0u);
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
     if (k >= c.K && k < kLzMRows - c.K && in_grid) {  // warp-uniform
         uint32_t *oA = c.dst + (size_t)z * c.chain_words + (ptrdiff_t)x * c.pitch;
         uint32_t *oB = oA + c.plane, *oC = oB + c.plane;
-        const bool sa = lane > 0 && wa >= 0 && wa < c.W, sb = lane < 31 && wb >= 0 && wb < c.W;
+        const bool sa = (lane > 0 || lclosed) && wa >= 0 && wa < c.W, sb = (lane < 31 || rclosed) && wb >= 0 && wb < c.W;
         if (sa && sb) {
             *reinterpret_cast<uint2 *>(oA + wa) = make_uint2(A.a, A.b);
             *reinterpret_cast<uint2 *>(oB + wa) = make_uint2(B.a, B.b);
@@ -1094,7 +1099,13 @@ int tsb_loz_create(int device, int sx, int sy, int nchains, const uint8_t *up, c
             for (int x = y * h->m_out; x < std::min(h->X, (y + 1) * h->m_out); ++x)
                 if (rg[x].y > rg[x].x) { lo = std::min(lo, rg[x].x); hi = std::max(hi, rg[x].y); }
             if (hi <= lo) continue;
-            for (int wa0 = (lo - 1) & ~1; wa0 + 1 < hi; wa0 += kLzWords) mt.push_back(make_int2(wa0, y));
+            // first tile from word 0 when the band starts there (it owns word 0);
+            // a tile reaching the grid's last word owns it (lz_multi_kernel)
+            for (int wa0 = lo == 0 ? 0 : (lo - 1) & ~1;; wa0 += kLzWords) {
+                mt.push_back(make_int2(wa0, y));
+                const int last = wa0 + kLzWords + (wa0 + 63 >= h->W - 1 ? 1 : 0);  // last owned word
+                if (last >= hi - 1) break;
+            }
         }
         h->nmtiles = (int)mt.size();
         if ((e = cudaMalloc(&h->mtiles, sizeof(int2) * std::max<size_t>(1, mt.size()))) != cudaSuccess)
