@@ -185,7 +185,10 @@ constexpr size_t sv_multi_smem() {
     return sizeof(uint32_t) * (2 * NW) * (32 * WPL + 1)  // rows (+ the east boundary word, XW tiles)
            + sizeof(uint64_t) * 32                      // lut
            + sizeof(uint32_t) * NW * (32 * WPL)         // per-warp flip words
-           + sizeof(uint16_t) * NW * (32 * WPL) * 16;   // per-warp job queues
+           + sizeof(uint16_t) * NW * (32 * WPL) * 16    // per-warp job queues
+           + sizeof(uint4) * NW * (32 * WPL)            // per-warp diagonal masks (nw, ne, sw, se)
+           + sizeof(uint32_t) * NW * (32 * WPL)         // per-warp local-minimum masks
+           + 16;                                        // alignment of the mask arrays
 }
 
 // XW: tiles of 32 * WPL words plus the read-only east boundary word (c.xw)
@@ -200,6 +203,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
     uint16_t *queue = reinterpret_cast<uint16_t *>(dsm + sizeof(uint32_t) * TR * RS + sizeof(uint64_t) * 32 +
                                                    sizeof(uint32_t) * NW * TW) +
                       (threadIdx.x >> 5) * TW * 16;
+    unsigned char *mbase = dsm + sizeof(uint32_t) * TR * RS + sizeof(uint64_t) * 32 + sizeof(uint32_t) * NW * TW +
+                           sizeof(uint16_t) * NW * TW * 16;
+    mbase += (16 - (size_t)(mbase - dsm) % 16) % 16;  // uint4 alignment
+    uint4 *dmask = reinterpret_cast<uint4 *>(mbase) + (threadIdx.x >> 5) * TW;
+    uint32_t *mnv = reinterpret_cast<uint32_t *>(mbase + sizeof(uint4) * NW * TW) + (threadIdx.x >> 5) * TW;
     const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
     const int z = blockIdx.z;
     const int r0 = (int)blockIdx.y * c.out_rows - c.K;  // even
@@ -330,43 +338,52 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             int pos = incl - cnt;
-            // job = li << 11 | lane << 6 | j << 4 | bit >> 1 (16 bits: a class sweep's sites all have
-            // bit parity pc);  li = (up ? 0 : 16) | nw<<3 | ne<<2 | sw<<1 | se
+            // job = lane << 6 | j << 4 | bit >> 1 (a class sweep's sites all have bit
+            // parity pc); the site's kind and LUT index are read from the warp's
+            // masks in shared memory by whichever lane draws its coin, so the
+            // serial per-lane queue loop stays short
+            const uint32_t head = (uint32_t)lane << 6;
 #pragma unroll
             for (int j = 0; j < WPL; ++j) {
-                for (uint32_t m = cand[j]; m; m &= m - 1) {
-                    const int bt = __ffs(m) - 1;
-                    const uint32_t li = (((mn[j] >> bt) & 1u) ? 0u : 16u) | (((nw[j] >> bt) & 1u) << 3) |
-                                        (((ne[j] >> bt) & 1u) << 2) | (((sw[j] >> bt) & 1u) << 1) |
-                                        ((se[j] >> bt) & 1u);
-                    queue[pos++] = (uint16_t)((li << 11) | ((uint32_t)lane << 6) | ((uint32_t)j << 4) | ((uint32_t)bt >> 1));
-                }
+                dmask[lane * WPL + j] = make_uint4(nw[j], ne[j], sw[j], se[j]);
+                mnv[lane * WPL + j] = mn[j];
+                for (uint32_t m = cand[j]; m; m &= m - 1)
+                    queue[pos++] = (uint16_t)(head | ((uint32_t)j << 4) | ((uint32_t)(__ffs(m) - 1) >> 1));
                 fres[lane * WPL + j] = 0u;
             }
             __syncwarp();
             const uint64_t salt = (step0 + (uint64_t)s + 1ull) * kGold;
             // site index R * f + 32 * (word) + bit, word = wl(lane 0) + lane' * WPL + j
             const uint64_t row_idx = (uint64_t)R * (uint64_t)c.f + (uint64_t)(int64_t)((wl - lane * WPL) * 32);
-            // high(x, job): u < p_high for the job's LUT entry
+            __syncwarp();
+            // high(x, w, b, up): u < p_high for site bit b of word w (up: a local minimum)
             auto deal = [&](auto high) {
                 for (int q = lane; q < total; q += 64) {
                     const bool two = q + 32 < total;
                     const uint32_t j0 = queue[q], j1 = two ? queue[q + 32] : j0;
                     const uint32_t w0 = ((j0 >> 6) & 31u) * WPL + ((j0 >> 4) & 3u), b0 = ((j0 & 15u) << 1) | (uint32_t)pc;
                     const uint32_t w1 = ((j1 >> 6) & 31u) * WPL + ((j1 >> 4) & 3u), b1 = ((j1 & 15u) << 1) | (uint32_t)pc;
+                    const uint32_t up0 = (mnv[w0] >> b0) & 1u, up1 = (mnv[w1] >> b1) & 1u;
                     const uint64_t i0 = row_idx + (uint64_t)(w0 * 32u + b0);
                     const uint64_t i1 = row_idx + (uint64_t)(w1 * 32u + b1);
                     const uint64_t x0 = mix64(mix64(base + (i0 + 1ull) * kGold) + salt);
                     const uint64_t x1 = mix64(mix64(base + (i1 + 1ull) * kGold) + salt);
                     // local min (up) moves iff u < p_high; local max moves iff u >= p_high
-                    if (high(x0, j0) == !((j0 >> 15) & 1u)) atomicOr(&fres[w0], 1u << b0);
-                    if (two && high(x1, j1) == !((j1 >> 15) & 1u)) atomicOr(&fres[w1], 1u << b1);
+                    if (high(x0, w0, b0, up0) == (bool)up0) atomicOr(&fres[w0], 1u << b0);
+                    if (two && high(x1, w1, b1, up1) == (bool)up1) atomicOr(&fres[w1], 1u << b1);
                 }
             };
-            if (c.half)  // p_high = 1/2: (x >> 11) < 2^52 iff bit 63 of x is 0
-                deal([](uint64_t x, uint32_t) { return (int32_t)(uint32_t)(x >> 32) >= 0; });
-            else
-                deal([&](uint64_t x, uint32_t j) { return (x >> 11) < lut[j >> 11]; });
+            if (c.half) {  // p_high = 1/2: (x >> 11) < 2^52 iff bit 63 of x is 0
+                deal([](uint64_t x, uint32_t, uint32_t, uint32_t) { return (int32_t)(uint32_t)(x >> 32) >= 0; });
+            } else {
+                // LUT index (up ? 0 : 16) | nw << 3 | ne << 2 | sw << 1 | se of the site
+                deal([&](uint64_t x, uint32_t w, uint32_t b, uint32_t up) {
+                    const uint4 dm = dmask[w];
+                    const uint32_t li = (up ? 0u : 16u) | (((dm.x >> b) & 1u) << 3) | (((dm.y >> b) & 1u) << 2) |
+                                        (((dm.z >> b) & 1u) << 1) | ((dm.w >> b) & 1u);
+                    return (x >> 11) < lut[li];
+                });
+            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < WPL; ++j) {
