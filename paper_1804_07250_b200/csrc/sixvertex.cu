@@ -294,18 +294,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
         // candidates (local minima and maxima) first; the rest of the fire
         // test -- which kind, the diagonal faces -- only in warps that have
         // candidates (the frozen bulk of an early state pays the masks alone)
-        uint32_t alleq[WPL], cand[WPL];
+        // a candidate's four neighbours are all equal to the centre or all
+        // different from it, i.e. equal to each other (the centre drops out)
+        uint32_t cand[WPL];
         int cnt = 0;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const uint32_t pb = j > 0 ? b[j - 1] : bL, nb = j < WPL - 1 ? b[j + 1] : bR;
             const uint32_t left = (b[j] << 1) | (pb >> 31), right = (b[j] >> 1) | (nb << 31);
-            const uint32_t eq_u = ~(u[j] ^ b[j]), eq_d = ~(d[j] ^ b[j]), eq_l = ~(left ^ b[j]),
-                           eq_r = ~(right ^ b[j]);
-            alleq[j] = eq_u & eq_d & eq_l & eq_r;
-            const uint32_t all_ne = ~(eq_u | eq_d | eq_l | eq_r);
             const uint32_t act = rowok ? (cm[j] & pcm & (j == 0 ? hmask_l : ~0u) & (j == WPL - 1 ? hmask_r : ~0u)) : 0u;
-            cand[j] = (alleq[j] | all_ne) & act;
+            cand[j] = ~((u[j] ^ d[j]) | (u[j] ^ left) | (u[j] ^ right)) & act;
             cnt += __popc(cand[j]);
         }
         if (__any_sync(0xffffffffu, cnt != 0)) {
@@ -324,7 +322,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) sv_multi_kernel(SvMCtx c) {
             for (int j = 0; j < WPL; ++j) {
                 const uint32_t pu = j > 0 ? u[j - 1] : uL, nu = j < WPL - 1 ? u[j + 1] : uR;
                 const uint32_t pd = j > 0 ? d[j - 1] : dL, nd = j < WPL - 1 ? d[j + 1] : dR;
-                mn[j] = odd ? cand[j] & ~alleq[j] : cand[j] & alleq[j];
+                mn[j] = cand[j] & (odd ? u[j] ^ b[j] : ~(u[j] ^ b[j]));  // neighbours one up
                 nw[j] = ((u[j] << 1) | (pu >> 31)) ^ b[j];
                 ne[j] = ((u[j] >> 1) | (nu << 31)) ^ b[j];
                 sw[j] = ((d[j] << 1) | (pd >> 31)) ^ b[j];
