@@ -270,8 +270,12 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         if (lane == 31) cmnext = 0u;
         const uint32_t d2a = (m.z >> 1) | (m.w << 31), d2b = (m.w >> 1) | (cmnext << 31);
         const uint32_t d4a = (B.a << 1) | (bprev >> 31), d4b = (B.b << 1) | (B.a >> 31);
-        const uint32_t lowa = B.a & m.x & C.a & ~A.a & ~d2a & ~d4a, lowb = B.b & m.y & C.b & ~A.b & ~d2b & ~d4b;
-        const uint32_t higha = A.a & d2a & d4a & ~B.a & ~m.x & ~C.a, highb = A.b & d2b & d4b & ~B.b & ~m.y & ~C.b;
+        // a rotateable star has (B, C, row-above A) all set and (A, d2, d4) all
+        // clear (low) or the reverse (high): the six bits agree once A, d2
+        // and d4 are inverted; low = rotateable with B set
+        const uint32_t stara = ~((B.a ^ m.x) | (B.a ^ C.a) | (B.a ^ ~A.a) | (B.a ^ ~d2a) | (B.a ^ ~d4a));
+        const uint32_t starb = ~((B.b ^ m.y) | (B.b ^ C.b) | (B.b ^ ~A.b) | (B.b ^ ~d2b) | (B.b ^ ~d4b));
+        const uint32_t lowa = stara & B.a, lowb = starb & B.b;
         // coins that cannot reach a stored bit are not drawn (as the domino
         // tiles): fire row x touches rows x-1 and x, so sweep s needs fire rows
         // s+1 .. kLzMRows-1-s, and a fire moves about one column per sweep, so
@@ -282,8 +286,8 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         // (a tile side closed by the grid edge has no stale halo: all its bits count)
         const uint32_t hl = lane == 0 && !lclosed ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
         const uint32_t hr = lane == 31 && !rclosed ? (reach >= 31 ? ~0u : (1u << (reach + 1)) - 1u) : ~0u;
-        const uint32_t rota = need ? (lowa | higha) & mod3_mask((b3a - cls + 3) % 3) & hl : 0u;
-        const uint32_t rotb = need ? (lowb | highb) & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
+        const uint32_t rota = need ? stara & mod3_mask((b3a - cls + 3) % 3) & hl : 0u;
+        const uint32_t rotb = need ? starb & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (rota | rotb) != 0u))
             f = warp_fire<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
