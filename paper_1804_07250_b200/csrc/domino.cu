@@ -201,11 +201,11 @@ __global__ void __launch_bounds__(32 * (kTileRows + 1), 3)
     const uint32_t act = ((r + color) & 1) ? 0xAAAAAAAAu : 0x55555555u;
     const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
     const uint32_t la = (cur.y << 1) | (hl >> 31);
-    const uint32_t ia = vua & cur.x & ~(la | cur.y);
-    const uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & (lane == 0 ? 0u : act);
     const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
-    const uint32_t ib = vub & cur.z & ~(lb | cur.w);
-    const uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & (lane == 31 ? act & 1u : act);
+    // rotateable (state 3 or 12): up, down, not-left, not-right agree; state 3 = rotateable with up set
+    const uint32_t ra = ~((vua ^ cur.x) | (vua ^ ~la) | (vua ^ ~cur.y)) & (lane == 0 ? 0u : act);
+    const uint32_t rb = ~((vub ^ cur.z) | (vub ^ ~lb) | (vub ^ ~cur.w)) & (lane == 31 ? act & 1u : act);
+    const uint32_t ia = vua, ib = vub;
     uint2 f = make_uint2(0u, 0u);
     if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
         const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
@@ -299,18 +299,19 @@ __device__ __forceinline__ void multi_tile(const SweepCtx &c, uint2 (*vs)[32], u
         // that are never stored (stale-halo argument above)
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.w, 1);
         const uint32_t la = (cur.y << 1) | (hl >> 31);
-        const uint32_t ia = vua & cur.x & ~(la | cur.y);
-        uint32_t ra = (ia | (~(vua | cur.x) & la & cur.y)) & act;
         const uint32_t lb = (cur.w << 1) | (cur.y >> 31);
-        const uint32_t ib = vub & cur.z & ~(lb | cur.w);
-        uint32_t rb = (ib | (~(vub | cur.z) & lb & cur.w)) & act;
+        // rotateable: state 3 (up and down edges crossed, left and right not)
+        // or 12 (the reverse), i.e. up, down, not-left and not-right agree;
+        // the state-3 sites are the rotateable ones with the up edge crossed
+        uint32_t ra = ~((vua ^ cur.x) | (vua ^ ~la) | (vua ^ ~cur.y)) & act;
+        uint32_t rb = ~((vub ^ cur.z) | (vub ^ ~lb) | (vub ^ ~cur.w)) & act;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (ra | rb) != 0u)) {
             // the masks only where coins are drawn: the frozen bulk never pays them
             ra &= need_a(s, k, lane);
             rb &= need_b(s, k, lane);
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
-            f = warp_fire<TM>(ra, rb, ia, ib, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step);
+            f = warp_fire<TM>(ra, rb, vua, vub, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, z, r, wa, step);
         }
         fs[k][lane] = f;
         __syncthreads();
@@ -465,8 +466,8 @@ __global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi1_kernel(Sw
         const uint32_t act = color ? ~act0 : act0;
         const uint32_t hl = __shfl_up_sync(0xffffffffu, cur.y, 1);  // lane 0: halo, wraps harmlessly
         const uint32_t la = (cur.y << 1) | (hl >> 31);
-        const uint32_t ia = vu & cur.x & ~(la | cur.y);
-        const uint32_t ra = (ia | (~(vu | cur.x) & la & cur.y)) & act;
+        const uint32_t ra = ~((vu ^ cur.x) | (vu ^ ~la) | (vu ^ ~cur.y)) & act;  // as multi_tile
+        const uint32_t ia = vu;
         uint32_t f = 0u;
         if (__any_sync(0xffffffffu, ra != 0u)) {
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
@@ -657,9 +658,11 @@ __global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi1c_kernel(S
         const uint32_t act = color ? ~act0 : act0;
         const uint32_t hlt = __shfl_up_sync(0xffffffffu, ct.y, 1), hlb = __shfl_up_sync(0xffffffffu, cb.y, 1);
         const uint32_t lat = (ct.y << 1) | (hlt >> 31), lab = (cb.y << 1) | (hlb >> 31);
-        const uint32_t iat = vut & ct.x & ~(lat | ct.y), iab = vub & cb.x & ~(lab | cb.y);
-        const uint32_t rat = (iat | (~(vut | ct.x) & lat & ct.y)) & act;
-        const uint32_t rab = (iab | (~(vub | cb.x) & lab & cb.y)) & act;
+        // as multi_tile: rotateable = the four edge bits agree (left, right
+        // inverted); state 3 = rotateable with the up edge crossed
+        const uint32_t rat = ~((vut ^ ct.x) | (vut ^ ~lat) | (vut ^ ~ct.y)) & act;
+        const uint32_t rab = ~((vub ^ cb.x) | (vub ^ ~lab) | (vub ^ ~cb.y)) & act;
+        const uint32_t iat = vut, iab = vub;
         const uint32_t un = rat | rab;
         uint32_t ft = 0u, fb = 0u;
         if (__any_sync(0xffffffffu, un != 0u)) {
