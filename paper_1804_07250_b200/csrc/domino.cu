@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(32 * kMRows, kMBlocks) domino_multi1c_kernel(S
             const uint64_t t = (TM == 1 && color) ? c.t1 : c.t0;
             // coin bits: 1 where u < p_up, on the union of both chains' sites
             const uint32_t cu =
-                warp_fire<TM, 1>(un, 0u, 0xFFFFFFFFu, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, zt, r,
+                warp_fire_body<TM, 1>(un, 0u, 0xFFFFFFFFu, 0u, queue[k], fres[k], c.seedinfo, c.tgrid, t, c.side, zt, r,
                                  wa, step).x;
             ft = rat & ~(cu ^ iat);
             fb = rab & ~(cu ^ iab);

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         const uint32_t rotb = need ? starb & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (rota | rotb) != 0u))
-            f = warp_fire<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
+            f = warp_fire_body<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
                               step0 + (uint64_t)s);
         fs[k][lane] = f;
         __syncthreads();
