@@ -286,8 +286,12 @@ __global__ void __launch_bounds__(32 * kLzMRows, MINB) lz_multi_kernel(LzMCtx c)
         // (a tile side closed by the grid edge has no stale halo: all its bits count)
         const uint32_t hl = lane == 0 && !lclosed ? (reach >= 32 ? ~0u : ~0u << (32 - reach)) : ~0u;
         const uint32_t hr = lane == 31 && !rclosed ? (reach >= 31 ? ~0u : (1u << (reach + 1)) - 1u) : ~0u;
-        const uint32_t rota = need ? stara & mod3_mask((b3a - cls + 3) % 3) & hl : 0u;
-        const uint32_t rotb = need ? starb & mod3_mask((b3b - cls + 3) % 3) & hr : 0u;
+        // bits b == k (mod 3) of a word: 0x49249249 << k (k = 0, 1, 2)
+        int ka = b3a - cls, kb = b3b - cls;
+        ka += ka < 0 ? 3 : 0;
+        kb += kb < 0 ? 3 : 0;
+        const uint32_t rota = need ? stara & (0x49249249u << ka) & hl : 0u;
+        const uint32_t rotb = need ? starb & (0x49249249u << kb) & hr : 0u;
         uint2 f = make_uint2(0u, 0u);
         if (__any_sync(0xffffffffu, (rota | rotb) != 0u))
             f = warp_fire_body<TM>(rota, rotb, lowa, lowb, queue[k], fres[k], c.seedinfo, c.tgrid, c.t0, c.Y, z, x, wa,
