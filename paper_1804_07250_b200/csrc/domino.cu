@@ -1083,8 +1083,19 @@ __device__ __forceinline__ void reorder_tiles(const unsigned *cost, const int2 *
     if (threadIdx.x == 0) tot_s = tot;
     __syncthreads();
     int cls[kOrderPer];
+    bool hot = false;
 #pragma unroll
-    for (int j = 0; j < kOrderPer; ++j) cls[j] = i0 + j < n ? cost_class(c[j], n, tot_s) : -1;
+    for (int j = 0; j < kOrderPer; ++j) {
+        cls[j] = i0 + j < n ? cost_class(c[j], n, tot_s) : -1;
+        hot |= cls[j] == kOrderClasses - 1;
+    }
+    // heavy-first pays only with a few hot tiles (a melting seam: some tile
+    // above 3x the mean); with a broad load (an equilibrium state) the
+    // band-major order interleaves heavy and light tiles on every SM
+    if (!__syncthreads_or(hot)) {
+#pragma unroll
+        for (int j = 0; j < kOrderPer; ++j) cls[j] = i0 + j < n ? 0 : -1;
+    }
     int pos = 0;  // block-uniform
     for (int k = kOrderClasses - 1; k >= 0; --k) {
         int cnt = 0;

@@ -31,7 +31,7 @@ struct tsb_domino {
     unsigned *m_cost = nullptr;   // last block duration per multi-sweep tile (cycles)
     int2 *m_perm = nullptr;       // mtiles in that order
     bool m_adapt = true;          // TSB_DOM_ADAPT=0: band-major order
-    int m_order_every = 4;        // reorder on every n-th graph replay (TSB_DOM_ORDER_EVERY)
+    int m_order_every = 8;        // reorder on every n-th graph replay (TSB_DOM_ORDER_EVERY)
     std::vector<int> mband_start;
     int win_m0 = 0, win_mn = 0;
     int win_rows = 0;  // rows of the swept window (set with the tile lists; default: side)
