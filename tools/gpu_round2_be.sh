@@ -1,0 +1,8 @@
+# Hot-tile rule at 5x the mean (libtsb_hot5.so) vs HEAD (3x).
+mkdir -p gpurun_out; rm -f gpurun_out/hot5_ab.txt
+L=paper_1804_07250_b200/_lib
+TSB_LIB=$PWD/$L/libtsb_hot5.so timeout 1800 python -m pytest tests/test_domino_gpu.py tests/test_collapse_gpu.py -q -x 2>&1 | tail -2 >> gpurun_out/hot5_ab.txt
+P='import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d["ms_per_step"],4), round(d["roofline"]["frac"],4), round(d["warm"]["us_per_sweep"],3), round(d["collapsed"]["us_per_sweep"],4), round(d["collapsed"]["warm"]["us_per_sweep"],3))'
+for rep in 1 2; do for lib in libtsb.so libtsb_hot5.so; do
+  echo "== $lib $(TSB_LIB=$PWD/$L/$lib timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline | python -c "$P")" >> gpurun_out/hot5_ab.txt
+done; done
