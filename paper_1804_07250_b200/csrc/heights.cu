@@ -487,9 +487,7 @@ int tsb_domino_heights(tsb_domino *h, int chain, int ref_r, int ref_c, int32_t *
     if (rc) return rc;
     int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
     if ((rc = domino_heights_dev(h, chain, ref_r, ref_c, dout, nullptr))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    TSB_CUDA(cudaStreamSynchronize(h->stream));
-    return TSB_OK;
+    return staged_d2h(out, dout, nv * sizeof(int32_t), h->stream);  // pinned staging, returns complete
 }
 
 int tsb_domino_height_sum_add(tsb_domino *h, int chain0, int n, int ref_r, int ref_c, long long *acc_dev) {

@@ -1300,9 +1300,7 @@ int tsb_loz_heights(tsb_loz *h, int chain, int ref_x, int ref_y, int32_t *out) {
     if (rc) return rc;
     int32_t *dout = reinterpret_cast<int32_t *>(h->bytes);
     if ((rc = lz_heights_dev(h, chain, ref_x, ref_y, dout, nullptr))) return rc;
-    TSB_CUDA(cudaMemcpyAsync(out, dout, nv * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    TSB_CUDA(cudaStreamSynchronize(h->stream));
-    return TSB_OK;
+    return staged_d2h(out, dout, nv * sizeof(int32_t), h->stream);  // pinned staging, returns complete
 }
 
 int tsb_loz_height_sum_add(tsb_loz *h, int chain0, int n, int ref_x, int ref_y, long long *acc_dev) {
